@@ -1,0 +1,575 @@
+// C-ABI implementation (include/vitdec_b200.h): validation with the
+// reference's exact messages, trellis construction, device dispatch, and the
+// host-buffer streaming engine (H2D / decode / D2H overlapped per device,
+// frames sharded across devices with no collective).
+#include "vitdec_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "vd_common.cuh"
+#include "vd_internal.h"
+
+struct vd_code {
+  int k = 0, b = 0, s = 0;
+  std::vector<std::uint32_t> polys;
+  std::vector<std::uint32_t> next, out, pred, in_out;
+  bool complement_paired = false;
+  mutable std::mutex mu;
+  mutable std::map<int, std::uint32_t*> dev_in_out;  // device -> uploaded in_out table
+  ~vd_code() {
+    for (auto& kv : dev_in_out) {
+      int prev = 0;
+      if (cudaGetDevice(&prev) == cudaSuccess && cudaSetDevice(kv.first) == cudaSuccess) {
+        cudaFree(kv.second);
+        cudaSetDevice(prev);
+      }
+    }
+  }
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+vd_status fail(vd_status st, const std::string& msg) {
+  g_err = msg;
+  return st;
+}
+
+vd_status cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear sticky-free errors
+  return fail(VD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define VD_CUDA(call, what)                         \
+  do {                                              \
+    const cudaError_t vd_e_ = (call);               \
+    if (vd_e_ != cudaSuccess) return cuda_fail(vd_e_, what); \
+  } while (0)
+
+// Trellis validation: messages of reference trellis.cpp:38-53.
+vd_status validate_spec(int k, int b, const std::uint32_t* polys) {
+  if (k < 2) return fail(VD_EINVAL, "constraint length must be >= 2");
+  if (b < 2) return fail(VD_EINVAL, "need at least 2 outputs per bit");
+  if (!polys) return fail(VD_EINVAL, "polynomial count must equal B");
+  if (k > 16) return fail(VD_EINVAL, "constraint length too large");
+  const std::uint32_t mask = (1u << k) - 1;
+  for (int i = 0; i < b; ++i) {
+    if (polys[i] == 0) return fail(VD_EINVAL, "zero generator polynomial");
+    if ((polys[i] & ~mask) != 0) return fail(VD_EINVAL, "generator polynomial wider than K bits");
+  }
+  return VD_OK;
+}
+
+// FrameConfig::validate, reference decoder.cpp:10-20.
+vd_status validate_cfg(const vd_frame_cfg* cfg, int period) {
+  if (!cfg) return fail(VD_EINVAL, "null frame config");
+  if (cfg->f < 1) return fail(VD_EINVAL, "frame size f must be >= 1");
+  if (cfg->v1 < 0 || cfg->v2 < 0) return fail(VD_EINVAL, "overlaps must be >= 0");
+  if (cfg->f0 < 0 || cfg->f0 > cfg->f) return fail(VD_EINVAL, "f0 must be in [0, f]");
+  if (period > 1 && (cfg->f % period || cfg->v1 % period || cfg->v2 % period)) {
+    return fail(VD_EINVAL, "f, v1 and v2 must be multiples of the puncture period");
+  }
+  if (cfg->start != VD_TB_STORED_MAX && cfg->start != VD_TB_RANDOM) {
+    return fail(VD_EINVAL, "unknown traceback start");
+  }
+  return VD_OK;
+}
+
+std::int64_t num_frames(const vd_frame_cfg* cfg, std::int64_t n) { return (n + cfg->f - 1) / cfg->f; }
+
+// Frames per output-word-aligned unit: L*f is a multiple of 32.
+std::int64_t align_unit(int f) {
+  int g = 32;
+  int x = f;
+  while (x) {
+    const int t = g % x;
+    g = x;
+    x = t;
+  }
+  return 32 / g;
+}
+
+vd_status check_gpu_envelope(const vd_code* code) {
+  if (code->k > 12) return fail(VD_EUNSUPPORTED, "GPU decoder supports K <= 12 (reference allows 16)");
+  if (code->b > 8) return fail(VD_EUNSUPPORTED, "GPU decoder supports B <= 8");
+  return VD_OK;
+}
+
+vd_status device_table(const vd_code* code, int device, const std::uint32_t** out) {
+  std::lock_guard<std::mutex> lk(code->mu);
+  auto it = code->dev_in_out.find(device);
+  if (it != code->dev_in_out.end()) {
+    *out = it->second;
+    return VD_OK;
+  }
+  std::uint32_t* d = nullptr;
+  VD_CUDA(cudaMalloc(&d, sizeof(std::uint32_t) * code->in_out.size()), "cudaMalloc(in_out)");
+  VD_CUDA(cudaMemcpy(d, code->in_out.data(), sizeof(std::uint32_t) * code->in_out.size(), cudaMemcpyHostToDevice),
+          "upload in_out");
+  code->dev_in_out[device] = d;
+  *out = d;
+  return VD_OK;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+vd_status resolve_device(int32_t device, int* out) {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    return fail(VD_ECUDA, "no CUDA device available (the decoder has no CPU fallback)");
+  }
+  if (device < 0) {
+    VD_CUDA(cudaGetDevice(out), "cudaGetDevice");
+    return VD_OK;
+  }
+  if (device >= count) return fail(VD_EINVAL, "device index out of range");
+  *out = device;
+  return VD_OK;
+}
+
+template <typename T>
+vd_status decode_device(const vd_code* code, const vd_frame_cfg* cfg, std::int64_t n, const T* llr,
+                        std::int64_t llr_stage0, std::int64_t fb, std::int64_t fe, std::uint32_t* out,
+                        std::int64_t out_stage0, void* sigma, std::int32_t device, void* stream) {
+  if (!code) return fail(VD_EINVAL, "null code");
+  if (vd_status st = validate_cfg(cfg, 1)) return st;
+  if (n < 1) return fail(VD_EINVAL, "empty llr block");
+  if (vd_status st = check_gpu_envelope(code)) return st;
+  const std::int64_t nf = num_frames(cfg, n);
+  if (fb < 0 || fe > nf || fb > fe) return fail(VD_EINVAL, "frame range out of bounds");
+  if (out_stage0 % 32 != 0) return fail(VD_EINVAL, "out_stage0 must be a multiple of 32");
+  if (fb == fe) return VD_OK;
+  if (!llr || !out) return fail(VD_EINVAL, "null buffer");
+  const vd::FrameGeom g0(fb, n, cfg->f, cfg->v1, cfg->v2, cfg->f0);
+  const vd::FrameGeom g1(fe - 1, n, cfg->f, cfg->v1, cfg->v2, cfg->f0);
+  if (llr_stage0 > g0.beg) return fail(VD_EINVAL, "llr window does not cover the frames' warm-up stages");
+  if (out_stage0 > g0.out_lo) return fail(VD_EINVAL, "output window starts after the first frame");
+
+  int dev = 0;
+  if (vd_status st = resolve_device(device, &dev)) return st;
+  DeviceGuard guard(dev);
+  const std::uint32_t* in_out = nullptr;
+  if (vd_status st = device_table(code, dev, &in_out)) return st;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  // Zero the output words the frames touch; kernels OR bits into them.
+  const std::int64_t w0 = (g0.out_lo - out_stage0) / 32;
+  const std::int64_t w1 = (g1.out_hi - out_stage0 + 31) / 32;
+  VD_CUDA(cudaMemsetAsync(out + w0, 0, sizeof(std::uint32_t) * (w1 - w0), s), "zero output");
+
+  vd::DecodeLaunch p;
+  p.k = code->k;
+  p.b = code->b;
+  p.s = code->s;
+  p.f = cfg->f;
+  p.v1 = cfg->v1;
+  p.v2 = cfg->v2;
+  p.f0 = cfg->f0;
+  p.start = cfg->start;
+  p.seed = cfg->seed;
+  p.n = n;
+  p.frame_begin = fb;
+  p.frame_end = fe;
+  p.llr = llr;
+  p.llr_stage0 = llr_stage0;
+  p.out = out;
+  p.out_stage0 = out_stage0;
+  p.sigma = sigma;
+  p.in_out = in_out;
+  for (int i = 0; i < code->b && i < 8; ++i) p.polys[i] = code->polys[i];
+  p.complement_paired = code->complement_paired;
+
+  cudaError_t e;
+  if constexpr (sizeof(T) == 1) {
+    if (vd::fast_path_supported(p)) {
+      e = vd::launch_fast_i8(p, s);
+    } else {
+      e = vd::launch_generic_i8(p, s);
+    }
+  } else {
+    e = vd::launch_generic_f64(p, s);
+  }
+  if (e == cudaErrorInvalidValue) return fail(VD_EUNSUPPORTED, "frame configuration exceeds the GPU kernel's shared-memory envelope");
+  if (e != cudaSuccess) return cuda_fail(e, "decode kernel launch");
+  return VD_OK;
+}
+
+// ---- host-buffer streaming engine ----------------------------------------
+
+struct DevCtx {
+  cudaStream_t st[2] = {nullptr, nullptr};
+  void* llr[2] = {nullptr, nullptr};
+  std::size_t llr_cap[2] = {0, 0};
+  std::uint32_t* out[2] = {nullptr, nullptr};
+  std::size_t out_cap[2] = {0, 0};
+};
+
+struct ThreadCtx {
+  std::map<int, DevCtx> devs;
+  ~ThreadCtx() {
+    for (auto& kv : devs) {
+      if (cudaSetDevice(kv.first) != cudaSuccess) continue;
+      for (int i = 0; i < 2; ++i) {
+        if (kv.second.llr[i]) cudaFree(kv.second.llr[i]);
+        if (kv.second.out[i]) cudaFree(kv.second.out[i]);
+        if (kv.second.st[i]) cudaStreamDestroy(kv.second.st[i]);
+      }
+    }
+  }
+};
+
+thread_local ThreadCtx tl_ctx;
+
+vd_status ensure(void** p, std::size_t* cap, std::size_t bytes) {
+  if (*cap >= bytes) return VD_OK;
+  if (*p) cudaFree(*p);
+  *p = nullptr;
+  *cap = 0;
+  VD_CUDA(cudaMalloc(p, bytes), "cudaMalloc(stream buffer)");
+  *cap = bytes;
+  return VD_OK;
+}
+
+struct Chunk {
+  std::int64_t f0, f1;  // frame range
+};
+
+template <typename T>
+vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr, std::int64_t n,
+                      std::uint32_t* out_packed, vd_stats* stats, const vd_exec* exec) {
+  if (!code) return fail(VD_EINVAL, "null code");
+  if (n < 1) return fail(VD_EINVAL, "empty llr block");
+  if (vd_status st = validate_cfg(cfg, 1)) return st;
+  if (stats) {
+    if (vd_status st = vd_frame_stats(cfg, n, stats)) return st;
+  }
+  if (vd_status st = check_gpu_envelope(code)) return st;
+  if (!llr || !out_packed) return fail(VD_EINVAL, "null buffer");
+
+  // Devices.
+  std::vector<int> devices;
+  {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      return fail(VD_ECUDA, "no CUDA device available (the decoder has no CPU fallback)");
+    }
+    const int want = (exec && exec->num_devices > 0) ? exec->num_devices : 0;
+    if (want == 0) {
+      int cur = 0;
+      VD_CUDA(cudaGetDevice(&cur), "cudaGetDevice");
+      devices.push_back(cur);
+    } else {
+      for (int i = 0; i < want; ++i) {
+        const int d = exec->devices ? exec->devices[i] : i;
+        if (d < 0 || d >= count) return fail(VD_EINVAL, "device index out of range");
+        devices.push_back(d);
+      }
+    }
+  }
+  const int nd = static_cast<int>(devices.size());
+  std::vector<std::int64_t> first(nd + 1);
+  if (vd_status st = vd_partition_frames(cfg, n, nd, first.data())) return st;
+
+  // Chunk plan: whole output-word-aligned units of frames per chunk.
+  const std::int64_t unit = align_unit(cfg->f);
+  std::int64_t chunk_stages = (exec && exec->chunk_stages > 0) ? exec->chunk_stages : (std::int64_t{1} << 24);
+  std::int64_t chunk_frames = std::max<std::int64_t>(unit, (chunk_stages / cfg->f) / unit * unit);
+  std::vector<std::vector<Chunk>> plan(nd);
+  std::size_t max_chunks = 0;
+  for (int d = 0; d < nd; ++d) {
+    for (std::int64_t c = first[d]; c < first[d + 1]; c += chunk_frames) {
+      plan[d].push_back({c, std::min(c + chunk_frames, first[d + 1])});
+    }
+    max_chunks = std::max(max_chunks, plan[d].size());
+  }
+  // Buffer sizes per device.
+  const std::int64_t max_window = std::min<std::int64_t>(chunk_frames * cfg->f + cfg->v1 + cfg->v2, n);
+  const std::size_t llr_bytes = sizeof(T) * static_cast<std::size_t>(max_window) * code->b;
+  const std::size_t out_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>((chunk_frames * cfg->f + 31) / 32 + 1);
+
+  for (int d = 0; d < nd; ++d) {
+    if (plan[d].empty()) continue;
+    DeviceGuard guard(devices[d]);
+    DevCtx& ctx = tl_ctx.devs[devices[d]];
+    for (int i = 0; i < 2; ++i) {
+      if (!ctx.st[i]) VD_CUDA(cudaStreamCreateWithFlags(&ctx.st[i], cudaStreamNonBlocking), "cudaStreamCreate");
+      if (vd_status st = ensure(&ctx.llr[i], &ctx.llr_cap[i], llr_bytes)) return st;
+      void* o = ctx.out[i];
+      if (vd_status st = ensure(&o, &ctx.out_cap[i], out_bytes)) return st;
+      ctx.out[i] = static_cast<std::uint32_t*>(o);
+    }
+  }
+
+  // Issue: chunk i of every device on that device's stream i % 2. Within a
+  // stream, the H2D of chunk i+2 is ordered after the kernel of chunk i.
+  for (std::size_t i = 0; i < max_chunks; ++i) {
+    for (int d = 0; d < nd; ++d) {
+      if (i >= plan[d].size()) continue;
+      DeviceGuard guard(devices[d]);
+      DevCtx& ctx = tl_ctx.devs[devices[d]];
+      const int slot = static_cast<int>(i & 1);
+      cudaStream_t s = ctx.st[slot];
+      const Chunk c = plan[d][i];
+      std::int64_t wb = 0, we = 0;
+      if (vd_status st = vd_frame_window(cfg, n, c.f0, c.f1, &wb, &we)) return st;
+      T* dl = static_cast<T*>(ctx.llr[slot]);
+      VD_CUDA(cudaMemcpyAsync(dl, llr + wb * code->b, sizeof(T) * (we - wb) * code->b, cudaMemcpyHostToDevice, s),
+              "H2D llr chunk");
+      const std::int64_t out_lo = c.f0 * cfg->f;  // multiple of 32 by construction
+      const std::int64_t out_hi = std::min<std::int64_t>(c.f1 * cfg->f, n);
+      vd_status st = decode_device<T>(code, cfg, n, dl, wb, c.f0, c.f1, ctx.out[slot], out_lo, nullptr, devices[d], s);
+      if (st != VD_OK) return st;
+      const std::int64_t words = (out_hi - out_lo + 31) / 32;
+      VD_CUDA(cudaMemcpyAsync(out_packed + out_lo / 32, ctx.out[slot], sizeof(std::uint32_t) * words,
+                              cudaMemcpyDeviceToHost, s),
+              "D2H packed bits");
+    }
+  }
+  for (int d = 0; d < nd; ++d) {
+    if (plan[d].empty()) continue;
+    DeviceGuard guard(devices[d]);
+    DevCtx& ctx = tl_ctx.devs[devices[d]];
+    for (int i = 0; i < 2; ++i) VD_CUDA(cudaStreamSynchronize(ctx.st[i]), "decode stream");
+  }
+  return VD_OK;
+}
+
+}  // namespace
+
+namespace vd {
+int sm_count() {
+  static std::mutex mu;
+  static std::map<int, int> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = cache.find(dev);
+  if (it != cache.end()) return it->second;
+  int n = 148;
+  if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) n = 148;
+  cache[dev] = n;
+  return n;
+}
+}  // namespace vd
+
+extern "C" {
+
+const char* vd_last_error(void) { return g_err.c_str(); }
+const char* vd_version(void) { return "vitdec_b200 0.1 (sm_100a)"; }
+
+vd_status vd_code_create(int32_t k, int32_t b, const uint32_t* polys, vd_code** out) {
+  if (!out) return fail(VD_EINVAL, "null output handle");
+  *out = nullptr;
+  if (vd_status st = validate_spec(k, b, polys)) return st;
+  auto c = std::make_unique<vd_code>();
+  c->k = k;
+  c->b = b;
+  c->s = 1 << (k - 1);
+  c->polys.assign(polys, polys + b);
+  const int s = c->s;
+  c->next.resize(2 * s);
+  c->out.resize(2 * s);
+  c->pred.assign(2 * s, 0);
+  c->in_out.assign(2 * s, 0);
+  // Tables as reference trellis.cpp:57-91.
+  for (std::uint32_t st = 0; st < static_cast<std::uint32_t>(s); ++st) {
+    for (std::uint32_t u = 0; u < 2; ++u) {
+      const std::uint32_t reg = (u << (k - 1)) | st;
+      std::uint32_t bo = 0;
+      for (int i = 0; i < b; ++i) bo |= static_cast<std::uint32_t>(__builtin_popcount(polys[i] & reg) & 1) << (b - 1 - i);
+      c->next[st * 2 + u] = (u << (k - 2)) | (st >> 1);
+      c->out[st * 2 + u] = bo;
+    }
+  }
+  const std::uint32_t low_mask = static_cast<std::uint32_t>(s / 2 - 1);
+  for (std::uint32_t j = 0; j < static_cast<std::uint32_t>(s); ++j) {
+    const std::uint32_t low = (s == 2) ? 0 : (j & low_mask);
+    const std::uint32_t u = j >> (k - 2);
+    for (std::uint32_t w = 0; w < 2; ++w) {
+      const std::uint32_t i = low * 2 + w;
+      c->pred[j * 2 + w] = i;
+      c->in_out[j * 2 + w] = c->out[i * 2 + u];
+    }
+  }
+  const std::uint32_t ones = (1u << b) - 1;
+  c->complement_paired = true;
+  for (int st = 0; st < s; ++st) {
+    if ((c->out[st * 2] ^ c->out[st * 2 + 1]) != ones) {
+      c->complement_paired = false;
+      break;
+    }
+  }
+  *out = c.release();
+  return VD_OK;
+}
+
+void vd_code_destroy(vd_code* code) { delete code; }
+int32_t vd_code_k(const vd_code* code) { return code ? code->k : 0; }
+int32_t vd_code_b(const vd_code* code) { return code ? code->b : 0; }
+
+vd_status vd_code_tables(const vd_code* code, uint32_t* next, uint32_t* out, uint32_t* pred, uint32_t* in_out,
+                         int32_t* complement_paired) {
+  if (!code) return fail(VD_EINVAL, "null code");
+  const std::size_t n = code->next.size();
+  if (next) std::memcpy(next, code->next.data(), n * sizeof(uint32_t));
+  if (out) std::memcpy(out, code->out.data(), n * sizeof(uint32_t));
+  if (pred) std::memcpy(pred, code->pred.data(), n * sizeof(uint32_t));
+  if (in_out) std::memcpy(in_out, code->in_out.data(), n * sizeof(uint32_t));
+  if (complement_paired) *complement_paired = code->complement_paired ? 1 : 0;
+  return VD_OK;
+}
+
+int32_t vd_code_fast_path(const vd_code* code) {
+  if (!code) return 0;
+  vd::DecodeLaunch p;
+  p.k = code->k;
+  p.b = code->b;
+  p.s = code->s;
+  p.f = 256;
+  p.v1 = p.v2 = 20;
+  p.n = 1 << 20;
+  for (int i = 0; i < code->b && i < 8; ++i) p.polys[i] = code->polys[i];
+  p.complement_paired = code->complement_paired;
+  return vd::fast_path_supported(p) ? 1 : 0;
+}
+
+vd_status vd_frame_cfg_validate(const vd_frame_cfg* cfg, int32_t pattern_period) {
+  return validate_cfg(cfg, pattern_period);
+}
+
+vd_status vd_frame_stats(const vd_frame_cfg* cfg, int64_t n, vd_stats* stats) {
+  if (vd_status st = validate_cfg(cfg, 1)) return st;
+  if (!stats) return fail(VD_EINVAL, "null stats");
+  // reference decoder.cpp:256-265 in closed form (O(1) instead of O(frames)):
+  // interior frames are identical; only the first ceil(v1/f) and the frames
+  // whose right overlap is clipped differ.
+  stats->frames = num_frames(cfg, n);
+  stats->stages = 0;
+  stats->tracebacks = 0;
+  const std::int64_t nf = stats->frames;
+  auto add = [&](std::int64_t m) {
+    const vd::FrameGeom g(m, n, cfg->f, cfg->v1, cfg->v2, cfg->f0);
+    stats->stages += g.len();
+    stats->tracebacks += g.num_sub;
+  };
+  const std::int64_t head = std::min<std::int64_t>(nf, (cfg->v1 + cfg->f - 1) / cfg->f + 1);
+  const std::int64_t tail_start = std::max<std::int64_t>(head, nf - ((cfg->v2 + cfg->f - 1) / cfg->f + 2));
+  for (std::int64_t m = 0; m < head; ++m) add(m);
+  if (tail_start > head) {
+    const vd::FrameGeom g(head, n, cfg->f, cfg->v1, cfg->v2, cfg->f0);
+    stats->stages += g.len() * (tail_start - head);
+    stats->tracebacks += g.num_sub * (tail_start - head);
+  }
+  for (std::int64_t m = tail_start; m < nf; ++m) add(m);
+  return VD_OK;
+}
+
+vd_status vd_partition_frames(const vd_frame_cfg* cfg, int64_t n, int32_t parts, int64_t* first) {
+  if (vd_status st = validate_cfg(cfg, 1)) return st;
+  if (parts < 1 || !first) return fail(VD_EINVAL, "bad partition request");
+  const std::int64_t nf = num_frames(cfg, n);
+  const std::int64_t unit = align_unit(cfg->f);
+  const std::int64_t units = (nf + unit - 1) / unit;
+  for (int p = 0; p <= parts; ++p) {
+    first[p] = std::min<std::int64_t>(nf, (units * p / parts) * unit);
+  }
+  first[parts] = nf;
+  return VD_OK;
+}
+
+vd_status vd_frame_window(const vd_frame_cfg* cfg, int64_t n, int64_t fb, int64_t fe, int64_t* begin, int64_t* end) {
+  if (vd_status st = validate_cfg(cfg, 1)) return st;
+  if (fb < 0 || fe <= fb || fe > num_frames(cfg, n)) return fail(VD_EINVAL, "frame range out of bounds");
+  const vd::FrameGeom g0(fb, n, cfg->f, cfg->v1, cfg->v2, cfg->f0);
+  const vd::FrameGeom g1(fe - 1, n, cfg->f, cfg->v1, cfg->v2, cfg->f0);
+  *begin = g0.beg;
+  *end = g1.end;
+  return VD_OK;
+}
+
+vd_status vd_decode_i8_device(const vd_code* code, const vd_frame_cfg* cfg, int64_t n, const int8_t* llr,
+                              int64_t llr_stage0, int64_t fb, int64_t fe, uint32_t* out, int64_t out_stage0,
+                              int64_t* sigma, int32_t device, void* stream) {
+  return decode_device<std::int8_t>(code, cfg, n, llr, llr_stage0, fb, fe, out, out_stage0, sigma, device, stream);
+}
+
+vd_status vd_decode_f64_device(const vd_code* code, const vd_frame_cfg* cfg, int64_t n, const double* llr,
+                               int64_t llr_stage0, int64_t fb, int64_t fe, uint32_t* out, int64_t out_stage0,
+                               double* sigma, int32_t device, void* stream) {
+  return decode_device<double>(code, cfg, n, llr, llr_stage0, fb, fe, out, out_stage0, sigma, device, stream);
+}
+
+vd_status vd_decode_i8(const vd_code* code, const vd_frame_cfg* cfg, const int8_t* llr, int64_t n, uint32_t* out,
+                       vd_stats* stats, const vd_exec* exec) {
+  return decode_host<std::int8_t>(code, cfg, llr, n, out, stats, exec);
+}
+
+vd_status vd_decode_f64(const vd_code* code, const vd_frame_cfg* cfg, const double* llr, int64_t n, uint32_t* out,
+                        vd_stats* stats, const vd_exec* exec) {
+  return decode_host<double>(code, cfg, llr, n, out, stats, exec);
+}
+
+vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n, uint32_t* out, vd_stats* stats,
+                               int32_t device) {
+  if (n < 1) return fail(VD_EINVAL, "empty llr block");
+  if (n > 0x7fffffffLL) return fail(VD_EUNSUPPORTED, "serial decode limited to 2^31-1 stages");
+  vd_frame_cfg cfg{};
+  cfg.f = static_cast<int32_t>(n);
+  vd_exec ex{};
+  int32_t dev = device;
+  if (device >= 0) {
+    ex.num_devices = 1;
+    ex.devices = &dev;
+  }
+  ex.chunk_stages = n;
+  return decode_host<double>(code, &cfg, llr, n, out, stats, &ex);
+}
+
+vd_status vd_synth_llr_i8_device(const vd_code* code, int64_t n, double sigma, double scale, uint64_t seed,
+                                 int8_t* llr, uint32_t* bits, int32_t device, void* stream) {
+  if (!code || !llr || n < 1) return fail(VD_EINVAL, "bad synth arguments");
+  if (code->b > 4) return fail(VD_EUNSUPPORTED, "synthetic generator supports B <= 4");
+  int dev = 0;
+  if (vd_status st = resolve_device(device, &dev)) return st;
+  DeviceGuard guard(dev);
+  const cudaError_t e = vd::launch_synth_i8(code->k, code->b, code->polys.data(), n, sigma, scale, seed, llr, bits,
+                                            static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "synth kernel");
+  return VD_OK;
+}
+
+vd_status vd_count_bit_errors_device(const uint32_t* a, const uint32_t* b, int64_t n_bits, unsigned long long* count,
+                                     int32_t device, void* stream) {
+  if (!a || !b || !count) return fail(VD_EINVAL, "null buffer");
+  int dev = 0;
+  if (vd_status st = resolve_device(device, &dev)) return st;
+  DeviceGuard guard(dev);
+  const cudaError_t e = vd::launch_count_bit_errors(a, b, n_bits, count, static_cast<cudaStream_t>(stream));
+  if (e != cudaSuccess) return cuda_fail(e, "bit-error count kernel");
+  return VD_OK;
+}
+
+}  // extern "C"

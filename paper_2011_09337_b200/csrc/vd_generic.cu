@@ -1,0 +1,262 @@
+// Generic unified Viterbi kernel for sm_100a: one warp per frame.
+//
+// This is the general-envelope path (any K in [2, 12], any B in [2, 8], any
+// code, int8 LLRs with int32 metrics or double LLRs with double metrics).
+// The throughput path for the benchmark codes is vd_fast.cu; this kernel
+// serves every other code/config on the GPU, the FP64 real-valued API, and
+// serial_decode's single long frame.
+//
+// Per frame (reference decode_frame, decoder.cpp:170-237), one warp:
+//   forward pass over the clipped window [beg, end):
+//     - stage table: lanes < 2^(B-1) evaluate branch_metric (decoder.cpp:22-30)
+//       in the reference's add order, the other half by complement symmetry
+//       (decoder.cpp:41-51);
+//     - ACS over the S states, lane j owning states j, j+32, ... with the
+//       reference's strict '>' (ties -> second predecessor, decoder.cpp:67-74);
+//     - decisions are warp ballots: one bit per state per stage, bit-packed
+//       32 states per word (shared memory when the frame fits, else a global
+//       scratch slot per warp);
+//     - argmax (lowest index on ties, decoder.cpp:80-90) at every subframe
+//       start stage (decoder.cpp:205-211);
+//   parallel traceback: subframe s is traced by lane s % 32
+//   (decoder.cpp:214-236); output bits are OR-ed into packed words.
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <type_traits>
+
+#include "vd_common.cuh"
+#include "vd_internal.h"
+
+namespace vd {
+namespace {
+
+constexpr int kWarps = 4;  // warps (frames in flight) per CTA
+constexpr unsigned kFull = 0xffffffffu;
+
+struct GenericParams {
+  DecodeLaunch p;
+  int words;           // decision words per stage = ceil(S / 32)
+  int len_max;         // max processed stages over the launched frames
+  int nsub_max;        // max subframes per frame
+  bool dec_in_smem;
+  std::uint32_t* dec_global;  // [total_warps][len_max * words] when !dec_in_smem
+  int smem_per_warp;          // bytes
+};
+
+template <typename M>
+__device__ __forceinline__ bool better(M v, int i, M bv, int bi) {
+  return v > bv || (v == bv && i < bi);
+}
+
+template <typename In, typename M>
+__global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParams gp) {
+  const DecodeLaunch& p = gp.p;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int S = p.s;
+  const int words = gp.words;
+  const std::uint32_t low_mask = static_cast<std::uint32_t>(S / 2 - 1);
+  const int nt = 1 << p.b;
+  const std::uint32_t half = 1u << (p.b - 1);
+  const std::uint32_t tmask = static_cast<std::uint32_t>(nt - 1);
+
+  unsigned char* base = smem_raw + static_cast<std::size_t>(warp) * gp.smem_per_warp;
+  M* sig0 = reinterpret_cast<M*>(base);
+  M* sig1 = sig0 + S;
+  M* table = sig1 + S;
+  int* start_state = reinterpret_cast<int*>(table + nt);
+  std::uint32_t* dec = reinterpret_cast<std::uint32_t*>(start_state + gp.nsub_max + (gp.nsub_max & 1));
+  const std::int64_t gwarp = static_cast<std::int64_t>(blockIdx.x) * kWarps + warp;
+  if (!gp.dec_in_smem) dec = gp.dec_global + gwarp * static_cast<std::int64_t>(gp.len_max) * words;
+
+  const In* llr = static_cast<const In*>(p.llr);
+  const std::int64_t total_warps = static_cast<std::int64_t>(gridDim.x) * kWarps;
+
+  for (std::int64_t m = p.frame_begin + gwarp; m < p.frame_end; m += total_warps) {
+    const FrameGeom g(m, p.n, p.f, p.v1, p.v2, p.f0);
+    const std::int64_t len = g.len();
+    M* sp = sig0;
+    M* sc = sig1;
+    for (int j = lane; j < S; j += 32) sp[j] = M(0);  // sigma_0 = 0 (decoder.cpp:195)
+    std::int64_t offset = 0;                            // int32 renormalisation offset
+    std::int64_t next_record = 0;
+    std::int64_t next_start = g.start_stage(0, p.v2);
+    __syncwarp();
+
+    for (std::int64_t t = 0; t < len; ++t) {
+      const In* lt = llr + (g.beg + t - p.llr_stage0) * p.b;
+      // Stage table (decoder.cpp:41-51): direct half, then complements.
+      for (std::uint32_t bo = lane; bo < half; bo += 32) {
+        M acc = M(0);
+        for (int i = 0; i < p.b; ++i) {
+          const M v = static_cast<M>(lt[i]);
+          acc += ((bo >> (p.b - 1 - i)) & 1u) ? -v : v;
+        }
+        table[bo] = acc;
+      }
+      __syncwarp();
+      for (std::uint32_t bo = half + lane; bo <= tmask; bo += 32) table[bo] = -table[bo ^ tmask];
+      __syncwarp();
+      // ACS (decoder.cpp:53-76).
+      for (int r = 0; r < words; ++r) {
+        const int j = r * 32 + lane;
+        bool d = false;
+        if (j < S) {
+          const std::uint32_t i1 = (static_cast<std::uint32_t>(j) & low_mask) << 1;
+          const M s1 = sp[i1] + table[__ldg(p.in_out + 2 * j)];
+          const M s2 = sp[i1 | 1] + table[__ldg(p.in_out + 2 * j + 1)];
+          d = !(s1 > s2);
+          sc[j] = d ? s2 : s1;
+        }
+        const std::uint32_t w = __ballot_sync(kFull, d);
+        if (lane == 0) dec[t * words + r] = w;
+      }
+      __syncwarp();
+      M* tmp = sp;
+      sp = sc;
+      sc = tmp;
+      if constexpr (std::is_integral<M>::value) {
+        // Keep int32 metrics far from overflow on long frames; the offset is
+        // re-added for metric export. Differences (hence decisions) are exact.
+        if ((t & 4095) == 4095) {
+          const M ref = sp[0];
+          __syncwarp();
+          for (int j = lane; j < S; j += 32) sp[j] -= ref;
+          offset += ref;
+          __syncwarp();
+        }
+      }
+      // Stored-max start states (decoder.cpp:205-211).
+      while (next_record < g.num_sub && next_start == t) {
+        M bv = sp[0];
+        int bi = 0;
+        bool have = false;
+        for (int j = lane; j < S; j += 32) {
+          if (!have || sp[j] > bv) {
+            bv = sp[j];
+            bi = j;
+            have = true;
+          }
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+          const M ov = __shfl_xor_sync(kFull, bv, o);
+          const int oi = __shfl_xor_sync(kFull, bi, o);
+          const bool oh = __shfl_xor_sync(kFull, have ? 1 : 0, o) != 0;
+          if (oh && (!have || better(ov, oi, bv, bi))) {
+            bv = ov;
+            bi = oi;
+            have = true;
+          }
+        }
+        if (lane == 0) start_state[next_record] = bi;
+        ++next_record;
+        if (next_record < g.num_sub) next_start = g.start_stage(next_record, p.v2);
+      }
+    }
+    __syncwarp();
+
+    if (p.sigma) {
+      for (int j = lane; j < S; j += 32) {
+        if constexpr (std::is_integral<M>::value) {
+          static_cast<std::int64_t*>(p.sigma)[(m - p.frame_begin) * S + j] = static_cast<std::int64_t>(sp[j]) + offset;
+        } else {
+          static_cast<double*>(p.sigma)[(m - p.frame_begin) * S + j] = sp[j];
+        }
+      }
+    }
+
+    // Parallel traceback (decoder.cpp:214-236): lane owns subframes s = lane mod 32.
+    for (std::int64_t s = lane; s < g.num_sub; s += 32) {
+      const std::int64_t st = g.start_stage(s, p.v2);
+      const std::int64_t lo = g.sub_lo(s), hi = g.sub_hi(s);
+      std::uint32_t state;
+      if (p.f0 > 0 && p.start == 1 && st < len - 1) {
+        state = static_cast<std::uint32_t>(mix_seed(p.seed, static_cast<std::uint64_t>(m) * 0x10001ull +
+                                                                static_cast<std::uint64_t>(s)) %
+                                           static_cast<std::uint64_t>(S));
+      } else {
+        state = static_cast<std::uint32_t>(start_state[s]);
+      }
+      std::uint32_t acc = 0;
+      std::int64_t cur = -1;
+      for (std::int64_t t = st; t >= lo - g.beg; --t) {
+        const std::int64_t stage = g.beg + t;
+        if (stage < hi) {
+          const std::int64_t rel = stage - p.out_stage0;
+          const std::int64_t w = rel >> 5;
+          if (w != cur) {
+            if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+            cur = w;
+            acc = 0;
+          }
+          acc |= (state >> (p.k - 2)) << (rel & 31);
+        }
+        const std::uint32_t d = (dec[t * words + (state >> 5)] >> (state & 31)) & 1u;
+        state = ((state & low_mask) << 1) | d;
+      }
+      if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+    }
+    __syncwarp();
+  }
+}
+
+template <typename In, typename M>
+cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
+  GenericParams gp;
+  gp.p = p;
+  gp.words = (p.s + 31) / 32;
+  // Upper bounds over all frames: the window is at most f + v1 + v2 stages
+  // (clipped to the stream) and a frame has at most ceil(f / f0) subframes.
+  const std::int64_t len_max = imin(static_cast<std::int64_t>(p.f) + p.v1 + p.v2, p.n);
+  const std::int64_t nsub_max = p.f0 > 0 ? (static_cast<std::int64_t>(p.f) + p.f0 - 1) / p.f0 : 1;
+  if (len_max > 0x7fffffffLL / gp.words) return cudaErrorInvalidValue;
+  gp.len_max = static_cast<int>(len_max);
+  gp.nsub_max = static_cast<int>(nsub_max);
+  const std::int64_t frames = p.frame_end - p.frame_begin;
+  if (frames <= 0) return cudaSuccess;
+
+  const std::size_t head = sizeof(M) * (2 * p.s + (1 << p.b)) + sizeof(int) * (gp.nsub_max + (gp.nsub_max & 1));
+  const std::size_t head_al = (head + 15) & ~std::size_t(15);
+  const std::size_t dec_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>(len_max) * gp.words;
+  constexpr std::size_t kSmemBudget = 200 * 1024;
+  gp.dec_in_smem = (head_al + dec_bytes) * kWarps <= kSmemBudget;
+  const std::size_t per_warp = gp.dec_in_smem ? head_al + dec_bytes : head_al;
+  if (per_warp * kWarps > kSmemBudget) return cudaErrorInvalidValue;  // K too large for this kernel
+  gp.smem_per_warp = static_cast<int>(per_warp);
+
+  std::int64_t blocks = (frames + kWarps - 1) / kWarps;
+  const int occ_blocks = sm_count() * 8;
+  if (blocks > occ_blocks) blocks = occ_blocks;
+  gp.dec_global = nullptr;
+  if (!gp.dec_in_smem) {
+    const std::size_t bytes = dec_bytes * static_cast<std::size_t>(blocks) * kWarps;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&gp.dec_global), bytes, stream);
+    if (e != cudaSuccess) return e;
+  }
+  const std::size_t smem = per_warp * kWarps;
+  auto kern = generic_kernel<In, M>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) {
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(gp);
+    e = cudaGetLastError();
+  }
+  if (gp.dec_global) {
+    const cudaError_t e2 = cudaFreeAsync(gp.dec_global, stream);
+    if (e == cudaSuccess) e = e2;
+  }
+  return e;
+}
+
+}  // namespace
+
+cudaError_t launch_generic_i8(const DecodeLaunch& p, cudaStream_t stream) {
+  return launch_generic<std::int8_t, std::int32_t>(p, stream);
+}
+
+cudaError_t launch_generic_f64(const DecodeLaunch& p, cudaStream_t stream) {
+  return launch_generic<double, double>(p, stream);
+}
+
+}  // namespace vd

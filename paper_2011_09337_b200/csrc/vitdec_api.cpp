@@ -1,0 +1,270 @@
+// The reference C++ decoder API (include/vitdec/{trellis,decoder}.hpp)
+// implemented over the vitdec_b200 C-ABI. This file replaces the reference's
+// trellis.cpp and decoder.cpp in a link: the decode entry points call the
+// GPU, everything else keeps the reference's semantics and exception
+// messages.
+#include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+#include <string>
+
+#include "vitdec/decoder.hpp"
+#include "vitdec/trellis.hpp"
+#include "vitdec_b200.h"
+
+namespace vitdec {
+namespace {
+
+[[noreturn]] void raise(vd_status st) {
+  const std::string msg = vd_last_error();
+  if (st == VD_EINVAL) throw std::invalid_argument(msg);
+  throw std::runtime_error("vitdec_b200: " + msg);
+}
+
+void check(vd_status st) {
+  if (st != VD_OK) raise(st);
+}
+
+vd_frame_cfg to_c(const FrameConfig& cfg) {
+  vd_frame_cfg c{};
+  c.f = cfg.f;
+  c.v1 = cfg.v1;
+  c.v2 = cfg.v2;
+  c.f0 = cfg.f0;
+  c.start = cfg.start == TracebackStart::kRandom ? VD_TB_RANDOM : VD_TB_STORED_MAX;
+  c.seed = cfg.seed;
+  return c;
+}
+
+DecodeStats from_c(const vd_stats& s) {
+  DecodeStats o;
+  o.frames = s.frames;
+  o.stages = s.stages;
+  o.tracebacks = s.tracebacks;
+  return o;
+}
+
+// reference decoder.cpp:92-97
+void check_block(const LlrBlock& llr, const Trellis& trellis) {
+  if (llr.cols() < 1) throw std::invalid_argument("empty llr block");
+  if (llr.rows() != trellis.outputs_per_bit()) throw std::invalid_argument("llr row count must equal B");
+}
+
+int env_gpus() {
+  const char* v = std::getenv("VITDEC_GPUS");
+  if (!v || !*v) return 1;
+  const int g = std::atoi(v);
+  return g > 0 ? g : 1;
+}
+
+// True when every value is an integer in [-127, 127]: the block is then
+// decoded by the int8 fixed-point kernels, exactly (integer sums are exact in
+// both the reference's double arithmetic and the kernel's int32 arithmetic).
+bool int8_exact(const LlrBlock& llr, std::vector<std::int8_t>* q) {
+  const Eigen::Index n = llr.size();
+  q->resize(static_cast<std::size_t>(n));
+  const double* d = llr.data();
+  for (Eigen::Index i = 0; i < n; ++i) {
+    const double v = d[i];
+    if (!(v >= -127.0 && v <= 127.0) || std::nearbyint(v) != v) return false;
+    (*q)[static_cast<std::size_t>(i)] = static_cast<std::int8_t>(v);
+  }
+  return true;
+}
+
+BitVec unpack(const std::vector<std::uint32_t>& packed, Eigen::Index n) {
+  BitVec bits(static_cast<std::size_t>(n));
+  for (Eigen::Index i = 0; i < n; ++i) bits[i] = static_cast<std::uint8_t>((packed[i >> 5] >> (i & 31)) & 1u);
+  return bits;
+}
+
+}  // namespace
+
+// ---- trellis.hpp ---------------------------------------------------------
+
+CodeSpec CodeSpec::from_octal(int k, const std::string& octal_csv) {
+  CodeSpec spec;
+  spec.k = k;
+  std::stringstream ss(octal_csv);
+  std::string tok;
+  while (std::getline(ss, tok, ',')) {
+    if (tok.empty()) continue;
+    std::size_t used = 0;
+    const unsigned long v = std::stoul(tok, &used, 8);
+    if (used != tok.size()) throw std::invalid_argument("bad octal polynomial: " + tok);
+    spec.polys.push_back(static_cast<std::uint32_t>(v));
+  }
+  spec.b = static_cast<int>(spec.polys.size());
+  return spec;
+}
+
+std::string CodeSpec::polys_octal() const {
+  std::ostringstream os;
+  for (std::size_t i = 0; i < polys.size(); ++i) os << (i ? "," : "") << std::oct << polys[i] << std::dec;
+  return os.str();
+}
+
+Trellis::Trellis(const CodeSpec& spec) : spec_(spec) {
+  // reference trellis.cpp:38-53 ordering: a polys/B count mismatch is
+  // reported before the C-ABI sees the (possibly short) array.
+  if (spec.k >= 2 && spec.b >= 2 && static_cast<int>(spec.polys.size()) != spec.b) {
+    throw std::invalid_argument("polynomial count must equal B");
+  }
+  vd_code* raw = nullptr;
+  std::vector<std::uint32_t> polys = spec.polys;
+  polys.resize(static_cast<std::size_t>(spec.b > 0 ? spec.b : 0), 0);
+  check(vd_code_create(spec.k, spec.b, polys.data(), &raw));
+  code_.reset(raw, vd_code_destroy);
+  num_states_ = 1 << (spec.k - 1);
+  const std::size_t n = static_cast<std::size_t>(num_states_) * 2;
+  next_.resize(n);
+  out_.resize(n);
+  pred_.resize(n);
+  in_out_.resize(n);
+  std::int32_t cp = 0;
+  check(vd_code_tables(raw, next_.data(), out_.data(), pred_.data(), in_out_.data(), &cp));
+  complement_paired_ = cp != 0;
+}
+
+Trellis build_trellis(const CodeSpec& spec) { return Trellis(spec); }
+
+// ---- decoder.hpp: configuration and per-stage helpers ----------------------
+
+void FrameConfig::validate(int pattern_period) const {
+  const vd_frame_cfg c = to_c(*this);
+  check(vd_frame_cfg_validate(&c, pattern_period));
+}
+
+// reference decoder.cpp:22-30 (sum in b order from 0.0)
+double branch_metric(std::uint32_t bo, const Eigen::Ref<const Eigen::ArrayXd>& llr_t) {
+  const int b = static_cast<int>(llr_t.size());
+  double m = 0.0;
+  for (int i = 0; i < b; ++i) m += ((bo >> (b - 1 - i)) & 1u) ? -llr_t[i] : llr_t[i];
+  return m;
+}
+
+// reference decoder.cpp:32-39
+Eigen::ArrayXd stage_metrics(const Eigen::Ref<const Eigen::ArrayXd>& llr_t) {
+  const int b = static_cast<int>(llr_t.size());
+  Eigen::ArrayXd half(Eigen::Index{1} << (b - 1));
+  for (Eigen::Index bo = 0; bo < half.size(); ++bo) half[bo] = branch_metric(static_cast<std::uint32_t>(bo), llr_t);
+  return half;
+}
+
+// reference decoder.cpp:41-51
+void fill_stage_table(const Eigen::Ref<const Eigen::ArrayXd>& llr_t, double* table) {
+  const int b = static_cast<int>(llr_t.size());
+  const std::uint32_t all = (1u << b) - 1;
+  for (std::uint32_t bo = 0; bo < (1u << (b - 1)); ++bo) table[bo] = branch_metric(bo, llr_t);
+  for (std::uint32_t bo = 1u << (b - 1); bo <= all; ++bo) table[bo] = -table[bo ^ all];
+}
+
+// reference decoder.cpp:53-76 (strict '>', ties to the second predecessor)
+void acs_stage(const Eigen::ArrayXd& sigma_prev, const double* stage_table, const Trellis& trellis,
+               Eigen::ArrayXd& sigma_cur, std::uint16_t* pi_col) {
+  const int s = trellis.num_states();
+  const std::uint32_t low = static_cast<std::uint32_t>(s / 2 - 1);
+  const std::uint32_t* io = trellis.incoming_output_data();
+  for (int j = 0; j < s; ++j) {
+    const std::uint32_t i1 = (static_cast<std::uint32_t>(j) & low) << 1;
+    const double a = sigma_prev[i1] + stage_table[io[2 * j]];
+    const double c = sigma_prev[i1 | 1] + stage_table[io[2 * j + 1]];
+    const bool second = !(a > c);
+    sigma_cur[j] = second ? c : a;
+    pi_col[j] = static_cast<std::uint16_t>(second ? (i1 | 1) : i1);
+  }
+}
+
+// reference decoder.cpp:131-163, without calling PuncturePattern's
+// out-of-line members (those live in the transmitter harness).
+LlrBlock depuncture(const Eigen::Ref<const Eigen::ArrayXd>& punctured, const PuncturePattern& p) {
+  if (p.b < 1 || p.period < 1 || static_cast<int>(p.mask.size()) != p.b * p.period) {
+    throw std::invalid_argument("puncture mask shape mismatch");
+  }
+  std::vector<int> kept(static_cast<std::size_t>(p.period), 0);
+  int per_period = 0;
+  for (int col = 0; col < p.period; ++col) {
+    for (int row = 0; row < p.b; ++row) kept[col] += p.at(row, col);
+    if (kept[col] == 0) throw std::invalid_argument("puncture mask drops an entire stage");
+    per_period += kept[col];
+  }
+  Eigen::Index rem = punctured.size();
+  Eigen::Index stages = (rem / per_period) * p.period;
+  rem %= per_period;
+  for (int col = 0; rem > 0; ++col) {
+    if (col >= p.period || rem < kept[col]) throw std::invalid_argument("punctured length inconsistent with pattern");
+    rem -= kept[col];
+    ++stages;
+  }
+  LlrBlock block = LlrBlock::Zero(p.b, stages);
+  Eigen::Index idx = 0;
+  for (Eigen::Index t = 0; t < stages; ++t) {
+    const int col = static_cast<int>(t % p.period);
+    for (int row = 0; row < p.b; ++row) {
+      if (p.at(row, col)) block(row, t) = punctured[idx++];
+    }
+  }
+  return block;
+}
+
+// ---- decoder.hpp: GPU decode entry points ---------------------------------
+
+DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const FrameConfig& cfg, int /*workers*/) {
+  check_block(llr, trellis);
+  cfg.validate();
+  const vd_frame_cfg c = to_c(cfg);
+  const Eigen::Index n = llr.cols();
+  std::vector<std::uint32_t> packed(static_cast<std::size_t>((n + 31) / 32));
+  vd_stats st{};
+  vd_exec ex{};
+  ex.num_devices = env_gpus();
+  std::vector<std::int8_t> q;
+  if (int8_exact(llr, &q)) {
+    check(vd_decode_i8(trellis.native(), &c, q.data(), n, packed.data(), &st, &ex));
+  } else {
+    check(vd_decode_f64(trellis.native(), &c, llr.data(), n, packed.data(), &st, &ex));
+  }
+  DecodeOutput out;
+  out.bits = unpack(packed, n);
+  out.stats = from_c(st);
+  return out;
+}
+
+DecodeOutput serial_decode(const LlrBlock& llr, const Trellis& trellis) {
+  check_block(llr, trellis);
+  const Eigen::Index n = llr.cols();
+  std::vector<std::uint32_t> packed(static_cast<std::size_t>((n + 31) / 32));
+  vd_stats st{};
+  std::vector<std::int8_t> q;
+  if (n <= 0x7fffffff && int8_exact(llr, &q)) {
+    // One frame covering the block with no overlap == serial_decode
+    // (reference acceptance.cpp:57-81 equivalence).
+    vd_frame_cfg c{};
+    c.f = static_cast<std::int32_t>(n);
+    vd_exec ex{};
+    ex.chunk_stages = n;
+    check(vd_decode_i8(trellis.native(), &c, q.data(), n, packed.data(), &st, &ex));
+  } else {
+    check(vd_serial_decode_f64(trellis.native(), llr.data(), n, packed.data(), &st, -1));
+  }
+  DecodeOutput out;
+  out.bits = unpack(packed, n);
+  out.stats = from_c(st);
+  return out;
+}
+
+DecodeStats framed_decode(const std::int8_t* llr, std::int64_t n_stages, const Trellis& trellis,
+                          const FrameConfig& cfg, std::uint32_t* packed_out, const ExecOptions& exec) {
+  cfg.validate();
+  const vd_frame_cfg c = to_c(cfg);
+  vd_stats st{};
+  vd_exec ex{};
+  ex.num_devices = exec.gpus > 0 ? exec.gpus : 1;
+  ex.chunk_stages = exec.chunk_stages;
+  check(vd_decode_i8(trellis.native(), &c, llr, n_stages, packed_out, &st, &ex));
+  return from_c(st);
+}
+
+}  // namespace vitdec

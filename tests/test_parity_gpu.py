@@ -1,0 +1,230 @@
+"""GPU parity: the sm_100a decode path vs the reference (golden vectors) and
+vs the CPU oracle, bit-exact, through the C-ABI.
+
+Bar: identical decoded bits and DecodeStats for the same
+int8 LLRs and frame configuration; identical final path metrics (integer
+metrics, renormalisation offset re-added); real-valued LLRs via the FP64
+kernel identical too. Full-size runs use size-independent properties
+(sampled-window parity, noiseless round trips, chunk/shard invariance).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2011_09337_b200 as vd
+from conftest import unpack
+
+pytestmark = pytest.mark.gpu
+
+K7 = (7, 2, [0o171, 0o133])
+
+
+def trellis(k, b, polys):
+    return vd.build_trellis(vd.CodeSpec(k, b, list(polys)))
+
+
+def block(stream, b):
+    """Stage-major stream -> B x N block (reference LlrBlock layout)."""
+    return np.asarray(stream).reshape(-1, b).T
+
+
+@pytest.fixture(scope="module")
+def port():
+    return oracle.port()
+
+
+def test_golden_framed_cases(golden):
+    meta, arr = golden
+    for c in meta["cases"]:
+        t = trellis(c["k"], c["b"], c["polys"])
+        cfg = vd.FrameConfig(**{k: v for k, v in c["cfg"].items() if k != "start"},
+                             start=vd.TracebackStart(c["cfg"]["start"]))
+        out = vd.framed_decode(block(arr[c["name"] + "_llr"], c["b"]), t, cfg)
+        assert np.array_equal(out.bits, unpack(arr[c["name"] + "_bits"], c["n"])), c["name"]
+        assert [out.stats.frames, out.stats.stages, out.stats.tracebacks] == c["stats"], c["name"]
+
+
+def test_golden_serial_cases(golden):
+    meta, arr = golden
+    for c in meta["serial"]:
+        t = trellis(c["k"], c["b"], c["polys"])
+        out = vd.serial_decode(block(arr[c["name"] + "_llr"], c["b"]), t)
+        assert np.array_equal(out.bits, unpack(arr[c["name"] + "_bits"], c["n"])), c["name"]
+        assert (out.stats.frames, out.stats.stages, out.stats.tracebacks) == (1, c["n"], 1)
+
+
+CODES = [(2, 2, [3, 1]), (3, 2, [7, 5]), (3, 2, [3, 5]), (3, 2, [6, 5]), (4, 3, [0o13, 0o15, 0o17]),
+         (5, 2, [0o23, 0o35]), (6, 4, [0o53, 0o75, 0o47, 0o71]), (7, 2, [0o171, 0o133]),
+         (7, 3, [0o133, 0o171, 0o165]), (8, 2, [0o247, 0o371]), (9, 2, [0o561, 0o753]),
+         (9, 3, [0o557, 0o663, 0o711]), (10, 2, [0o1167, 0o1545])]
+
+
+@pytest.mark.parametrize("code", CODES, ids=lambda c: f"K{c[0]}B{c[1]}")
+def test_random_configs_vs_oracle(code, port):
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng(1000 + k * 10 + b)
+    for it in range(10):
+        n = int(rng.integers(1, 5000))
+        f = int(rng.integers(1, 400))
+        cfg = vd.FrameConfig(f, int(rng.integers(0, 80)), int(rng.integers(0, 80)), int(rng.integers(0, f + 1)),
+                             vd.TracebackStart(int(rng.integers(0, 2))), int(rng.integers(0, 2**63)))
+        scale = [32.0, 4.0, 1.0][it % 3]
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(-1, 4)), int(rng.integers(0, 2**32)))
+        llr = oracle.quantize(rx, scale) if it < 7 else rx
+        exp, st, _ = port.framed_decode(k, b, polys, llr, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        out = vd.framed_decode(block(llr, b), t, cfg)
+        assert np.array_equal(out.bits, exp), (k, b, n, cfg, scale)
+        assert (out.stats.frames, out.stats.stages, out.stats.tracebacks) == st
+
+
+def test_headline_config_c1(port):
+    """Config 1: K=7 r1/2, 1M info bits at 3 dB, int8 scale 32 — both frame
+    configurations of the minimum slice."""
+    n = 1_000_000
+    rx, sent = port.gen_bench_block(*K7, n, 3.0, 1)
+    q = oracle.quantize(rx, 32.0)
+    t = trellis(*K7)
+    for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 45, 32)):
+        exp, st, _ = port.framed_decode(*K7, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0)
+        packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+        assert np.array_equal(vd.unpack_bits(packed, n), exp)
+        assert (stats.frames, stats.stages, stats.tracebacks) == st
+        assert np.count_nonzero(exp != sent) < n * 1e-3  # sane BER at 3 dB
+
+
+def test_path_metric_parity(port):
+    """Final per-frame path metrics of the int8 kernel == oracle's doubles."""
+    import torch
+
+    for k, b, polys in [K7, (9, 2, [0o561, 0o753]), (7, 3, [0o133, 0o171, 0o165]), (3, 2, [7, 5])]:
+        n = 6000
+        rx, _ = port.gen_bench_block(k, b, polys, n, 2.0, 17)
+        q = oracle.quantize(rx, 32.0)
+        for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(100, 13, 45, 32), vd.FrameConfig(n, 0, 0)):
+            _, _, sig = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, want_sigma=True)
+            nf = -(-n // cfg.f)
+            t = trellis(k, b, polys)
+            llr = torch.from_numpy(q).cuda()
+            out = torch.zeros((n + 31) // 32 + 1, dtype=torch.int32, device="cuda")
+            sigma = torch.zeros((nf, 1 << (k - 1)), dtype=torch.int64, device="cuda")
+            from paper_2011_09337_b200.device import decode_i8_device
+
+            decode_i8_device(t, cfg, n, llr, 0, 0, nf, out, 0, sigma)
+            torch.cuda.synchronize()
+            assert np.array_equal(sigma.cpu().numpy().astype(np.float64), sig), (k, cfg)
+
+
+def test_fp64_path_is_bit_exact_on_real_llrs(port):
+    rng = np.random.default_rng(7)
+    for k, b, polys in [K7, (9, 2, [0o561, 0o753]), (4, 3, [0o13, 0o15, 0o17])]:
+        n = 3000
+        llr = rng.standard_normal(n * b) * 1.7
+        for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(128, 20, 40, 32, vd.TracebackStart.kRandom, 9)):
+            exp, st, _ = port.framed_decode(k, b, polys, llr, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start),
+                                            cfg.seed)
+            out = vd.framed_decode(block(llr, b), trellis(k, b, polys), cfg)
+            assert np.array_equal(out.bits, exp)
+        assert np.array_equal(vd.serial_decode(block(llr, b), trellis(k, b, polys)).bits,
+                              port.serial_decode(k, b, polys, llr, n))
+
+
+def test_chunking_and_shard_invariance(port):
+    """Output is identical for any streaming chunk size and for frame-range
+    shards decoded separately (the multi-GPU decomposition, on one device)."""
+    import torch
+
+    from paper_2011_09337_b200.device import decode_i8_device
+
+    n = 200_003
+    rx, _ = port.gen_bench_block(*K7, n, 2.5, 99)
+    q = oracle.quantize(rx)
+    t = trellis(*K7)
+    for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(100, 30, 45, 25, vd.TracebackStart.kRandom, 4)):
+        exp, _, _ = port.framed_decode(*K7, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        for chunk in (0, 4096, 50_000):
+            packed, _ = vd.framed_decode_stream(q, n, t, cfg, chunk_stages=chunk)
+            assert np.array_equal(vd.unpack_bits(packed, n), exp), chunk
+        for parts in (2, 3, 8):
+            first = vd.partition_frames(cfg, n, parts)
+            merged = np.zeros((n + 31) // 32, np.uint32)
+            for a, bnd in zip(first, first[1:]):
+                if a == bnd:
+                    continue
+                lo, hi = vd.frame_window(cfg, n, a, bnd)
+                llr = torch.from_numpy(q[lo * 2:hi * 2].copy()).cuda()  # only this shard's halo window
+                out0 = (a * cfg.f) // 32 * 32
+                words = (min(bnd * cfg.f, n) - out0 + 31) // 32
+                out = torch.zeros(words, dtype=torch.int32, device="cuda")
+                decode_i8_device(t, cfg, n, llr, lo, a, bnd, out, out0)
+                torch.cuda.synchronize()
+                merged[out0 // 32:out0 // 32 + words] |= out.cpu().numpy().view(np.uint32)
+            assert np.array_equal(vd.unpack_bits(merged, n), exp), parts
+
+
+def test_large_stream_sampled_windows(port):
+    """2^25-stage synthetic stream decoded on device; frames in sampled
+    windows must equal an oracle decode of just that window re-based to the
+    frame grid."""
+    import torch
+
+    from paper_2011_09337_b200.device import decode_i8_device, synth_llr_i8
+
+    n = 1 << 25
+    t = trellis(*K7)
+    cfg = vd.FrameConfig(256, 20, 20)
+    llr = torch.empty(n * 2, dtype=torch.int8, device="cuda")
+    bits = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+    synth_llr_i8(t, n, 0.7071, 32.0, 123, llr, bits)
+    nf = n // cfg.f
+    out = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
+    decode_i8_device(t, cfg, n, llr, 0, 0, nf, out, 0)
+    torch.cuda.synchronize()
+    got = out.cpu().numpy().view(np.uint32)
+    host_llr = llr.cpu().numpy()
+    rng = np.random.default_rng(3)
+    for m0 in [0, nf - 8, *rng.integers(1, nf - 8, 6).tolist()]:
+        m1 = m0 + 8
+        origin = max(m0 - 1, 0) * cfg.f  # ceil(v1/f) = 1 frame of lead-in
+        end = min(m1 * cfg.f + cfg.v2, n)
+        sub = host_llr[origin * 2:end * 2]
+        exp, _, _ = port.framed_decode(*K7, sub, end - origin, cfg.f, cfg.v1, cfg.v2)
+        lo, hi = m0 * cfg.f - origin, m1 * cfg.f - origin
+        assert np.array_equal(vd.unpack_bits(got, n)[origin + lo:origin + hi], exp[lo:hi]), m0
+    # decoded vs sent: sane BER at 3 dB
+    errs = np.unpackbits((got ^ bits.cpu().numpy().view(np.uint32)).view(np.uint8)).sum()
+    assert errs < n * 1e-3
+
+
+def test_ber_sweep_counts_match_reference(golden, port):
+    """Config 2 parity: the reference run_ber_sweep recipe (berlab.cpp:42-99)
+    with the GPU decoding each 65536-bit block reproduces the reference's own
+    error counts exactly (unquantised doubles -> FP64 kernel)."""
+    meta, _ = golden
+    for sw in meta["ber_sweeps"]:
+        t = trellis(*K7)
+        for p, ebn0 in enumerate(sw["ebn0"]):
+            sigma = port.sigma_from_ebn0(ebn0, 0.5)
+            errors = 0
+            nblk = -(-sw["bits_per_point"] // sw["block_bits"])
+            for blk in range(nblk):
+                n = min(sw["block_bits"], sw["bits_per_point"] - blk * sw["block_bits"])
+                rx, sent = port.gen_sweep_block(*K7, n, sigma, port.mix_seed(sw["seed"], p * 0x100000 + blk))
+                if sw["frame"] is None:
+                    bits = vd.serial_decode(block(rx, 2), t).bits
+                else:
+                    f, v1, v2, f0, start, seed = sw["frame"]
+                    bits = vd.framed_decode(block(rx, 2), t,
+                                            vd.FrameConfig(f, v1, v2, f0, vd.TracebackStart(start), seed)).bits
+                errors += int(np.count_nonzero(bits != sent))
+            assert errors == sw["errors"][p], (sw["frame"], ebn0)
+
+
+def test_error_behaviour_on_gpu():
+    t = trellis(*K7)
+    with pytest.raises(ValueError, match="empty llr block"):
+        vd.framed_decode(np.zeros((2, 0)), t, vd.FrameConfig(f=4))
+    with pytest.raises(ValueError, match="frame size f must be >= 1"):
+        vd.framed_decode(np.zeros((2, 10)), t, vd.FrameConfig(f=0))
+    with pytest.raises(ValueError, match="llr row count must equal B"):
+        vd.serial_decode(np.zeros((3, 10)), t)
