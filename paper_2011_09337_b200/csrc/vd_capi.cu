@@ -451,6 +451,8 @@ int32_t vd_code_fast_path(const vd_code* code) {
   p.f = 256;
   p.v1 = p.v2 = 20;
   p.n = 1 << 20;
+  p.frame_begin = 0;
+  p.frame_end = p.n / p.f;
   for (int i = 0; i < code->b && i < 8; ++i) p.polys[i] = code->polys[i];
   p.complement_paired = code->complement_paired;
   return vd::fast_path_supported(p) ? 1 : 0;

@@ -222,7 +222,7 @@ cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
   const std::size_t dec_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>(len_max) * gp.words;
   constexpr std::size_t kSmemBudget = 200 * 1024;
   gp.dec_in_smem = (head_al + dec_bytes) * kWarps <= kSmemBudget;
-  const std::size_t per_warp = gp.dec_in_smem ? head_al + dec_bytes : head_al;
+  const std::size_t per_warp = ((gp.dec_in_smem ? head_al + dec_bytes : head_al) + 15) & ~std::size_t(15);
   if (per_warp * kWarps > kSmemBudget) return cudaErrorInvalidValue;  // K too large for this kernel
   gp.smem_per_warp = static_cast<int>(per_warp);
 

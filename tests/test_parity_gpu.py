@@ -228,3 +228,53 @@ def test_error_behaviour_on_gpu():
         vd.framed_decode(np.zeros((2, 10)), t, vd.FrameConfig(f=0))
     with pytest.raises(ValueError, match="llr row count must equal B"):
         vd.serial_decode(np.zeros((3, 10)), t)
+
+
+FAST_CODES = [(7, 2, [0o171, 0o133]), (7, 2, [0o133, 0o171]), (9, 2, [0o561, 0o753]), (9, 2, [0o753, 0o561]),
+              (5, 2, [0o23, 0o35]), (6, 2, [0o53, 0o75]), (8, 2, [0o247, 0o371])]
+
+
+@pytest.mark.parametrize("code", FAST_CODES, ids=lambda c: f"K{c[0]}_{c[2][0]:o}")
+def test_fast_path_vs_oracle(code, port):
+    """The register-resident kernel (interior frames) + generic kernel (edge
+    frames) against the oracle over many frame configurations."""
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    assert t.fast_path(), "fast path should serve this code"
+    rng = np.random.default_rng(2000 + k)
+    cfgs = [vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 45, 32), vd.FrameConfig(64, 16, 24, 16),
+            vd.FrameConfig(128, 20, 40, 32, vd.TracebackStart.kRandom, 5), vd.FrameConfig(100, 14, 30, 30),
+            vd.FrameConfig(512, 42, 42), vd.FrameConfig(32, 0, 35), vd.FrameConfig(64, 64, 0, 1)]
+    for i, cfg in enumerate(cfgs):
+        n = int(rng.integers(60_000, 120_000))
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(0, 4)), 77 + i)
+        q = oracle.quantize(rx, [32.0, 4.0][i % 2])
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+        got = vd.unpack_bits(packed, n)
+        bad = np.flatnonzero(got != exp)
+        assert bad.size == 0, (k, cfg, n, bad[:10], bad.size)
+        assert (stats.frames, stats.stages, stats.tracebacks) == st
+
+
+def test_fast_path_metrics(port):
+    import torch
+
+    from paper_2011_09337_b200.device import decode_i8_device
+
+    for k, b, polys in [K7, (9, 2, [0o561, 0o753])]:
+        n = 50_000
+        rx, _ = port.gen_bench_block(k, b, polys, n, 2.0, 3)
+        q = oracle.quantize(rx, 32.0)
+        t = trellis(k, b, polys)
+        for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 46, 32)):
+            _, _, sig = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, want_sigma=True)
+            nf = -(-n // cfg.f)
+            llr = torch.from_numpy(q).cuda()
+            out = torch.zeros((n + 31) // 32 + 1, dtype=torch.int32, device="cuda")
+            sigma = torch.zeros((nf, 1 << (k - 1)), dtype=torch.int64, device="cuda")
+            decode_i8_device(t, cfg, n, llr, 0, 0, nf, out, 0, sigma)
+            torch.cuda.synchronize()
+            got = sigma.cpu().numpy().astype(np.float64)
+            bad = np.flatnonzero(np.any(got != sig, axis=1))
+            assert bad.size == 0, (k, cfg, bad[:5])
