@@ -117,22 +117,116 @@ struct FastParams {
   int dec_off, x_off, ss_off;  // byte offsets of the regions inside a warp's area
 };
 
-// Per-lane, per-phase LLR flip constants (folds the lane part of the branch
-// index into the metric table, see header).
+// Opaque copy: keeps a per-lane constant in a register instead of letting the
+// compiler rematerialise it from threadIdx every block.
+__device__ __forceinline__ std::uint32_t opaque(std::uint32_t x) {
+  asm volatile("" : "+r"(x));
+  return x;
+}
+
+// (a & m) | (b & ~m) as one LOP3 that the compiler cannot re-associate into a
+// serial chain (keeps the decision-compaction tree 3 deep).
+template <std::uint32_t MASK>
+__device__ __forceinline__ std::uint32_t bitsel(std::uint32_t a, std::uint32_t b) {
+  std::uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(MASK));  // 0xE4: c ? a : b
+  return r;
+}
+
+// 32 decisions (16 registers x 2 frames) -> one word, bit (rho + 16 * half).
+__device__ __forceinline__ std::uint32_t compact16(const std::uint32_t* w) {
+  std::uint32_t y[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) y[q] = prmt(w[q], w[q + 8], 0xFBD9u);
+  const std::uint32_t a = bitsel<0x01010101u>(y[0], y[1]);
+  const std::uint32_t b = bitsel<0x04040404u>(y[2], y[3]);
+  const std::uint32_t c = bitsel<0x10101010u>(y[4], y[5]);
+  const std::uint32_t d = bitsel<0x40404040u>(y[6], y[7]);
+  const std::uint32_t ab = bitsel<0x03030303u>(a, b);
+  const std::uint32_t cd = bitsel<0x30303030u>(c, d);
+  return bitsel<0x0f0f0f0fu>(ab, cd);
+}
+
 template <class GEO>
-struct PhaseConsts {
-  std::uint32_t fm[GEO::LB];  // XOR mask on the gathered (l0A, l1A, l0B, l1B) bytes
-  std::uint32_t k0[GEO::LB];  // exactness corrections for the flipped bytes
-  std::uint32_t k1[GEO::LB];
+struct FrameState {
+  std::uint32_t sig[GEO::R];
+  std::uint32_t wv[2][GEO::R];
+  std::uint32_t fm[GEO::LB], k0[GEO::LB], k1[GEO::LB];  // per-lane LLR flip constants per phase
+  std::uint32_t cur[2][GEO::LB / 2];                     // LLR words of this block (frame A, B)
+  std::uint32_t nxt[2][GEO::LB / 2];                     // and of the next block
 };
+
+struct BlockCtx {
+  int v1, L;
+  std::uint32_t* drow_lane;  // dec + lane
+  int dummy_row;             // row index receiving out-of-range decision words
+};
+
+// One block of LB stages. SLOW adds the per-stage range checks and the
+// stored-max argmax hook; FAST blocks (fully inside the stored range, no
+// argmax) are straight-line code.
+template <class C, class GEO, bool SLOW, class RecFn>
+__device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev, RecFn&& rec) {
+  constexpr int LB = GEO::LB, R = GEO::R;
+  constexpr std::uint32_t BIAS = 0x80008000u;
+  constexpr std::uint32_t OFF2 = 0x02000200u;
+  // ---- branch-metric tables for the LB stages of this block (both frames) ---
+  std::uint32_t PT[LB][4], CL[LB][4];
+#pragma unroll
+  for (int k = 0; k < LB; ++k) {
+    const std::uint32_t wA = st.cur[0][k >> 1], wB = st.cur[1][k >> 1];
+    const std::uint32_t o = (k & 1) * 2;
+    const std::uint32_t sel = o | ((o + 1) << 4) | ((o + 4) << 8) | ((o + 5) << 12);
+    const std::uint32_t tmp = prmt(wA, wB, sel) ^ st.fm[k];
+    const std::uint32_t X = prmt(tmp, 0u, 0x4240u);  // (L0A, L0B) offset-binary, zero-extended
+    const std::uint32_t Y = prmt(tmp, 0u, 0x4341u);  // (L1A, L1B)
+    PT[k][0] = X + Y + st.k0[k];                     // T0 + 256 = l0 + l1 + 256
+    PT[k][1] = X + (Y ^ 0x00ff00ffu) + st.k1[k];     // T1 + 256 = l0 - l1 + 256
+    PT[k][3] = OFF2 - PT[k][0];                      // T3 = -T0
+    PT[k][2] = OFF2 - PT[k][1];                      // T2 = -T1
+#pragma unroll
+    for (int x = 0; x < 4; ++x) CL[k][x] = PT[k][x ^ 3] - PT[k][x] + BIAS;
+  }
+#pragma unroll
+  for (int k = 0; k < LB; ++k) {
+    const int t = blk * LB + k;
+    std::uint32_t* w = st.wv[k & 1];
+    // ---- add-compare-select, in place: E/O registers differ in bit k -------
+#pragma unroll
+    for (int e = 0; e < R; ++e) {
+      if ((e >> k) & 1) continue;
+      const int od = e | (1 << k);
+      const std::uint32_t x = GEO::xreg(k, e);
+      const std::uint32_t sE = st.sig[e], sO = st.sig[od];
+      const std::uint32_t s2L = __vadd2(sO, PT[k][x ^ 3]);
+      const std::uint32_t s2H = __vadd2(sO, PT[k][x]);
+      w[e] = sO - sE + CL[k][x];
+      w[od] = sO - sE + CL[k][x ^ 3];
+      st.sig[e] = __viaddmax_s16x2(sE, PT[k][x], s2L);
+      st.sig[od] = __viaddmax_s16x2(sE, PT[k][x ^ 3], s2H);
+    }
+    // ---- previous stage's decisions -> shared memory (overlaps this ACS) ---
+    const std::uint32_t word = compact16(st.wv[(k + 1) & 1]);
+    if constexpr (SLOW) {
+      const int row = (tprev >= bc.v1 && tprev < bc.L) ? tprev - bc.v1 : bc.dummy_row;
+      bc.drow_lane[row * 32] = word;
+      tprev = t;
+      rec(t, k);
+    } else {
+      bc.drow_lane[(t - 1 - bc.v1) * 32] = word;
+    }
+  }
+  if constexpr (!SLOW) tprev = blk * LB + LB - 1;
+}
 
 template <class C, int R>
 __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
   using GEO = Geo<C, R>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, r = GEO::r, g = GEO::g;
-  constexpr std::uint32_t BASE = 0x20002000u;     // offset-binary metric origin (8192 per half)
-  constexpr std::uint32_t BIAS = 0x80008000u;     // decision-bit bias
-  constexpr std::uint32_t OFF2 = 0x02000200u;     // 2 * 256: table complement origin
+  constexpr std::uint32_t BASE = 0x20002000u;  // offset-binary metric origin (8192 per half)
+  constexpr int WPB = LB / 2;
+  static_assert(LB % 2 == 0, "B=2 fast path needs an even block length");
+  static_assert(R == 16, "one 32-bit decision word per lane per stage");
   const DecodeLaunch& p = fp.p;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -159,8 +253,8 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
   const std::uint32_t* llrB = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
                                                                      (lB * f - v1 - p.llr_stage0) * 2);
 
-  // Per-phase flip constants for this lane.
-  PhaseConsts<GEO> pc;
+  FrameState<GEO> st;
+  // Per-phase flip constants for this lane (lane part of the branch index).
 #pragma unroll
   for (int k = 0; k < LB; ++k) {
     std::uint32_t z = 0;
@@ -169,172 +263,154 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
       if ((lam >> i) & 1) z ^= C::cb(r + i - k);
     }
     const std::uint32_t f0b = (z >> 1) & 1u, f1b = z & 1u;  // flip l0 / flip l1
-    pc.fm[k] = 0x80808080u ^ (f0b ? 0x00ff00ffu : 0u) ^ (f1b ? 0xff00ff00u : 0u);
-    pc.k0[k] = (f0b + f1b) * 0x00010001u;
-    pc.k1[k] = (f0b + 1u - f1b) * 0x00010001u;
+    st.fm[k] = opaque(0x80808080u ^ (f0b ? 0x00ff00ffu : 0u) ^ (f1b ? 0xff00ff00u : 0u));
+    st.k0[k] = opaque((f0b + f1b) * 0x00010001u);
+    st.k1[k] = opaque((f0b + 1u - f1b) * 0x00010001u);
   }
-
-  std::uint32_t sig[R];
 #pragma unroll
-  for (int i = 0; i < R; ++i) sig[i] = BASE;
+  for (int i = 0; i < R; ++i) st.sig[i] = BASE;
+#pragma unroll
+  for (int i = 0; i < R; ++i) st.wv[1][i] = 0u;
   std::int32_t subA = 0, subB = 0;  // accumulated renormalisation (ref - BASE) per half
 
-  // LLR words: LB stages x 2 bytes = LB/2 words per frame per block.
-  constexpr int WPB = LB / 2;
-  static_assert(LB % 2 == 0, "B=2 fast path needs an even block length");
-  std::uint32_t curA[WPB], curB[WPB], nxtA[WPB], nxtB[WPB];
 #pragma unroll
   for (int i = 0; i < WPB; ++i) {
-    curA[i] = __ldg(llrA + i);
-    curB[i] = __ldg(llrB + i);
-    nxtA[i] = __ldg(llrA + WPB + i);
-    nxtB[i] = __ldg(llrB + WPB + i);
+    st.cur[0][i] = __ldg(llrA + i);
+    st.cur[1][i] = __ldg(llrB + i);
+    st.nxt[0][i] = __ldg(llrA + WPB + i);
+    st.nxt[1][i] = __ldg(llrB + WPB + i);
   }
+  const std::uint32_t* pfA = llrA + 2 * WPB;
+  const std::uint32_t* pfB = llrB + 2 * WPB;
 
   int next_sub = 0;
   // subframes whose traceback starts from the stored max state
   auto sub_start = [&](int s) { return v1 + min((s + 1) * fp.step, f) + v2 - 1; };
   auto needs_record = [&](int s) {
-    const int st = sub_start(s);
-    return !(p.f0 > 0 && p.start == 1 && st < L - 1);
+    const int sst = sub_start(s);
+    return !(p.f0 > 0 && p.start == 1 && sst < L - 1);
   };
   while (next_sub < fp.num_sub && !needs_record(next_sub)) ++next_sub;
   int next_rec = next_sub < fp.num_sub ? sub_start(next_sub) : 0x7fffffff;
 
+  // stored-max argmax at start stages (decoder.cpp:205-211)
+  auto rec = [&](int t, int k) {
+    if (t != next_rec) return;
+    // key = (metric << 16) | (0xFFFF - state): max -> best metric, lowest state.
+    const int sh = (k + 1) % M;
+    const std::uint32_t lanepart =
+        ((static_cast<std::uint32_t>(lam * R) >> sh) | (static_cast<std::uint32_t>(lam * R) << (M - sh))) &
+        GEO::SMASK;
+    std::uint32_t bestA = 0, bestB = 0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      const std::uint32_t regpart = static_cast<std::uint32_t>(GEO::rotr(i, k + 1));
+      const std::uint32_t ck = (lanepart | regpart) ^ 0xffffu;
+      bestA = max(bestA, prmt(ck, st.sig[i], 0x5410u));
+      bestB = max(bestB, prmt(ck, st.sig[i], 0x7610u));
+    }
+#pragma unroll
+    for (int o2 = 1; o2 < G; o2 <<= 1) {
+      bestA = max(bestA, __shfl_xor_sync(kFull, bestA, o2));
+      bestB = max(bestB, __shfl_xor_sync(kFull, bestB, o2));
+    }
+    if (lam == 0) {
+      sstate[(2 * grp) * fp.num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestA & 0xffffu));
+      sstate[(2 * grp + 1) * fp.num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestB & 0xffffu));
+    }
+    if (t == L - 1 && p.sigma != nullptr) {
+      // final metrics: true = stored - BASE - 256 * L + sum(ref - BASE)
+      std::int64_t* sg = static_cast<std::int64_t*>(p.sigma);
+#pragma unroll
+      for (int i = 0; i < R; ++i) {
+        const int sidx = static_cast<int>(lanepart | static_cast<std::uint32_t>(GEO::rotr(i, k + 1)));
+        const std::int64_t a = static_cast<std::int64_t>(st.sig[i] & 0xffffu) - 8192 - 256LL * L + subA;
+        const std::int64_t b = static_cast<std::int64_t>(st.sig[i] >> 16) - 8192 - 256LL * L + subB;
+        if (validA) sg[(mA - p.frame_begin) * S + sidx] = a;
+        if (validB) sg[(mB - p.frame_begin) * S + sidx] = b;
+      }
+    }
+    ++next_sub;
+    while (next_sub < fp.num_sub && !needs_record(next_sub)) ++next_sub;
+    next_rec = next_sub < fp.num_sub ? sub_start(next_sub) : 0x7fffffff;
+  };
+
+  BlockCtx bc;
+  bc.v1 = v1;
+  bc.L = L;
+  bc.drow_lane = dec + lane;
+  bc.dummy_row = f + v2;  // one spare row after the stored range
+  int tprev = -1;
+
   for (int blk = 0; blk < fp.nblk; ++blk) {
     const int t0 = blk * LB;
-#pragma unroll
-    for (int k = 0; k < LB; ++k) {
-      const int t = t0 + k;
-      // ---- branch-metric tables for this stage (both frames) -------------
-      const std::uint32_t wA = curA[k >> 1], wB = curB[k >> 1];
-      const std::uint32_t o = (k & 1) * 2;
-      const std::uint32_t sel = o | ((o + 1) << 4) | ((o + 4) << 8) | ((o + 5) << 12);
-      const std::uint32_t tmp = prmt(wA, wB, sel) ^ pc.fm[k];
-      const std::uint32_t X = prmt(tmp, 0u, 0x4240u);  // (L0A, L0B) offset-binary, zero-extended
-      const std::uint32_t Y = prmt(tmp, 0u, 0x4341u);  // (L1A, L1B)
-      std::uint32_t PT[4], CL[4];
-      PT[0] = X + Y + pc.k0[k];                         // T0 + 256 = l0 + l1 + 256
-      PT[1] = X + (Y ^ 0x00ff00ffu) + pc.k1[k];         // T1 + 256 = l0 - l1 + 256
-      PT[3] = OFF2 - PT[0];                             // T3 = -T0
-      PT[2] = OFF2 - PT[1];                             // T2 = -T1
-#pragma unroll
-      for (int x = 0; x < 4; ++x) CL[x] = PT[x ^ 3] - PT[x] + BIAS;
-      // ---- add-compare-select, in place, E/O registers differ in bit k -----
-      std::uint32_t w[R];
-#pragma unroll
-      for (int e = 0; e < R; ++e) {
-        if ((e >> k) & 1) continue;
-        const int od = e | (1 << k);
-        const std::uint32_t x = GEO::xreg(k, e);
-        const std::uint32_t sE = sig[e], sO = sig[od];
-        const std::uint32_t s2L = __vadd2(sO, PT[x ^ 3]);
-        const std::uint32_t s2H = __vadd2(sO, PT[x]);
-        w[e] = sO - sE + CL[x];
-        w[od] = sO - sE + CL[x ^ 3];
-        sig[e] = __viaddmax_s16x2(sE, PT[x], s2L);
-        sig[od] = __viaddmax_s16x2(sE, PT[x ^ 3], s2H);
-      }
-      // ---- decision compaction: 2R decisions -> R/16 words ------------------
-      if (t >= v1 && t < L) {  // only stages a traceback can reach are stored
-#pragma unroll
-        for (int wd = 0; wd < R / 16; ++wd) {
-          std::uint32_t m = prmt(w[16 * wd], w[16 * wd + 1], 0xFDB9u);
-#pragma unroll
-          for (int q = 1; q < 8; ++q) {
-            const std::uint32_t y = prmt(w[16 * wd + 2 * q], w[16 * wd + 2 * q + 1], 0xFDB9u);
-            const std::uint32_t MQ = 0x01010101u * ((1u << q) - 1u);
-            m = (m & MQ) | (y & ~MQ);
-          }
-          dec[((t - v1) * (R / 16) + wd) * 32 + lane] = m;
-        }
-      }
-      // ---- stored-max start states (decoder.cpp:205-211) -------------------
-      if (t == next_rec) {
-        // key = (metric << 16) | (0xFFFF - state): max -> best metric, lowest state.
-        const int sh = (k + 1) % M;
-        const std::uint32_t lanepart =
-            ((static_cast<std::uint32_t>(lam * R) >> sh) | (static_cast<std::uint32_t>(lam * R) << (M - sh))) &
-            GEO::SMASK;
-        std::uint32_t bestA = 0, bestB = 0;
-#pragma unroll
-        for (int i = 0; i < R; ++i) {
-          const std::uint32_t regpart = static_cast<std::uint32_t>(GEO::rotr(i, k + 1));
-          const std::uint32_t ck = (lanepart | regpart) ^ 0xffffu;
-          const std::uint32_t ka = prmt(ck, sig[i], 0x5410u);
-          const std::uint32_t kb = prmt(ck, sig[i], 0x7610u);
-          bestA = max(bestA, ka);
-          bestB = max(bestB, kb);
-        }
-#pragma unroll
-        for (int o2 = 1; o2 < G; o2 <<= 1) {
-          bestA = max(bestA, __shfl_xor_sync(kFull, bestA, o2));
-          bestB = max(bestB, __shfl_xor_sync(kFull, bestB, o2));
-        }
-        if (lam == 0) {
-          sstate[(2 * grp) * fp.num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestA & 0xffffu));
-          sstate[(2 * grp + 1) * fp.num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestB & 0xffffu));
-        }
-        if (t == L - 1 && p.sigma != nullptr) {
-          // final metrics: true = stored - BASE - 256 * L + sum(ref - BASE)
-          std::int64_t* sg = static_cast<std::int64_t*>(p.sigma);
-#pragma unroll
-          for (int i = 0; i < R; ++i) {
-            const int st = static_cast<int>(lanepart | static_cast<std::uint32_t>(GEO::rotr(i, k + 1)));
-            const std::int64_t a = static_cast<std::int64_t>(sig[i] & 0xffffu) - 8192 - 256LL * L + subA;
-            const std::int64_t b = static_cast<std::int64_t>(sig[i] >> 16) - 8192 - 256LL * L + subB;
-            if (validA) sg[(mA - p.frame_begin) * S + st] = a;
-            if (validB) sg[(mB - p.frame_begin) * S + st] = b;
-          }
-        }
-        ++next_sub;
-        while (next_sub < fp.num_sub && !needs_record(next_sub)) ++next_sub;
-        next_rec = next_sub < fp.num_sub ? sub_start(next_sub) : 0x7fffffff;
-      }
+    // fast block: every pending store (stages t0-1 .. t0+LB-2) is in range and
+    // no start stage falls inside the block
+    const bool fast = (t0 - 1 >= v1) && (t0 + LB - 2 < L) && !(next_rec >= t0 && next_rec < t0 + LB);
+    if (fast) {
+      run_block<C, GEO, false>(st, blk, bc, tprev, rec);
+    } else {
+      run_block<C, GEO, true>(st, blk, bc, tprev, rec);
     }
     // ---- LLR pipeline: advance one block, prefetch the block after next ----
 #pragma unroll
     for (int i = 0; i < WPB; ++i) {
-      curA[i] = nxtA[i];
-      curB[i] = nxtB[i];
-      nxtA[i] = __ldg(llrA + (blk + 2) * WPB + i);
-      nxtB[i] = __ldg(llrB + (blk + 2) * WPB + i);
+      st.cur[0][i] = st.nxt[0][i];
+      st.cur[1][i] = st.nxt[1][i];
+      st.nxt[0][i] = __ldg(pfA + i);
+      st.nxt[1][i] = __ldg(pfB + i);
     }
+    pfA += WPB;
+    pfB += WPB;
     // ---- renormalisation every 2 blocks (group-wide reference) ------------
     if (blk & 1) {
-      const std::uint32_t ref = __shfl_sync(kFull, sig[0], grp * G);
+      const std::uint32_t ref = __shfl_sync(kFull, st.sig[0], grp * G);
       subA += static_cast<std::int32_t>(ref & 0xffffu) - 8192;
       subB += static_cast<std::int32_t>(ref >> 16) - 8192;
 #pragma unroll
-      for (int i = 0; i < R; ++i) sig[i] = sig[i] - ref + BASE;
+      for (int i = 0; i < R; ++i) st.sig[i] = st.sig[i] - ref + BASE;
     }
     // ---- relayout: back to the canonical layout (P_new = rotr(P_old, r)) --
     if constexpr (g > 0) {
       std::uint32_t* xb = xbuf + grp * GEO::XSTRIDE;
 #pragma unroll
-      for (int i = 0; i < R; ++i) xb[(i << g) | lam] = sig[i];
+      for (int i = 0; i < R; ++i) xb[(i << g) | lam] = st.sig[i];
       __syncwarp();
       const uint4* src = reinterpret_cast<const uint4*>(xb + lam * R);
 #pragma unroll
       for (int i = 0; i < R / 4; ++i) {
         const uint4 v = src[i];
-        sig[4 * i] = v.x;
-        sig[4 * i + 1] = v.y;
-        sig[4 * i + 2] = v.z;
-        sig[4 * i + 3] = v.w;
+        st.sig[4 * i] = v.x;
+        st.sig[4 * i + 1] = v.y;
+        st.sig[4 * i + 2] = v.z;
+        st.sig[4 * i + 3] = v.w;
       }
       __syncwarp();
     }
   }
+  // decisions of the last processed stage
+  {
+    const std::uint32_t word = compact16(st.wv[(fp.nblk * LB - 1) & 1]);
+    const int row = (tprev >= v1 && tprev < L) ? tprev - v1 : bc.dummy_row;
+    bc.drow_lane[row * 32] = word;
+  }
   __syncwarp();
 
   // ---- subframe-parallel traceback (decoder.cpp:214-236) --------------------
-  const int ntask = 2 * fp.num_sub;
-  for (int task = lam; task < ntask; task += G) {
-    const int half = task & 1;
-    const int s = task >> 1;
-    const std::int64_t m = half ? mB : mA;
-    if (!(half ? validB : validA)) continue;
+  // Tasks (frame, subframe) are spread over all 32 lanes of the warp, frames
+  // fastest: in a round every lane traces one task, reading any group's
+  // decision words from shared memory. Within a block of LB stages the lane
+  // index of the traced state (P >> r) is fixed (only register bits are
+  // rewritten), so the block's words are fetched together: one shared-memory
+  // latency per LB steps, and the per-step work is branch-free.
+  const int ntask = GEO::FPW * fp.num_sub;
+  for (int task = lane; task - lane < ntask; task += 32) {
+    const bool active = task < ntask;
+    const int fr = active ? task % GEO::FPW : 0;  // frame slot in the warp (2 * group + half)
+    const int s = active ? task / GEO::FPW : 0;
+    const int half = fr & 1;
+    const std::int64_t m = mbase + fr;
+    const bool valid = active && m < fp.mi1;
     const int st = sub_start(s);
     const int sub_lo = v1 + s * fp.step;
     const int sub_hi = v1 + min((s + 1) * fp.step, f);
@@ -344,41 +420,63 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
                                                               static_cast<std::uint64_t>(s)) %
                                          static_cast<std::uint64_t>(S));
     } else {
-      state = sstate[(2 * grp + half) * fp.num_sub + s];
+      state = sstate[fr * fp.num_sub + s];
     }
-    int k = st % LB;
-    // physical index after stage st: rotl(state, k + 1)
-    const int sh = (k + 1) % M;
+    // physical index after stage st (phase st % LB): rotl(state, phase + 1)
+    const int sh = ((st & (LB - 1)) + 1) % M;
     std::uint32_t P = sh == 0 ? state : (((state << sh) | (state >> (M - sh))) & GEO::SMASK);
+    const std::uint32_t hsh = half ? 16u : 0u;
+    const std::uint32_t* gdec = dec + (fr >> 1) * G;  // this frame's group columns
     const std::int64_t obase = m * f - v1 - p.out_stage0;  // output bit index of frame-relative stage 0
     std::uint32_t acc = 0;
-    std::int64_t cur = -1;
-    const std::uint32_t* drow = dec + (grp * G);
-    for (int t = st; t >= sub_lo; --t) {
+    int nb = 0;
+    int t = st;
+    while (t >= sub_lo) {
+      const int tb0 = t & ~(LB - 1);
       const std::uint32_t lp = P >> r;
-      const std::uint32_t rho = P & (R - 1);
-      const std::uint32_t word = drow[((t - v1) * (R / 16) + (rho >> 4)) * 32 + lp];
-      const std::uint32_t bit = 8u * (2u * (rho & 1u) + half) + ((rho >> 1) & 7u);
-      const std::uint32_t d = (word >> bit) & 1u;
-      if (t < sub_hi) {
-        const std::int64_t ob = obase + t;
-        const std::int64_t wi = ob >> 5;
-        if (wi != cur) {
-          if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
-          cur = wi;
+      std::uint32_t wd[LB];
+#pragma unroll
+      for (int j = 0; j < LB; ++j) {
+        const int row = max(tb0 + j - v1, 0);
+        wd[j] = gdec[row * 32 + lp];
+      }
+#pragma unroll
+      for (int j = LB - 1; j >= 0; --j) {
+        const int sj = tb0 + j;
+        const bool in = sj <= t && sj >= sub_lo;
+        const std::uint32_t dbit = (wd[j] >> ((P & (R - 1)) | hsh)) & 1u;
+        const bool em = in && sj < sub_hi;
+        const std::uint32_t ob = (P >> j) & 1u;
+        acc = em ? ((acc << 1) | ob) : acc;
+        nb += em ? 1 : 0;
+        const std::uint32_t Pn = (P & ~(1u << j)) | (dbit << j);
+        P = in ? Pn : P;
+        if (nb == 32) {
+          const std::int64_t ol = obase + sj;  // lowest output index held in acc
+          const std::int64_t w0 = ol >> 5;
+          const int o = static_cast<int>(ol & 31);
+          if (valid) {
+            if (o == 0) {
+              p.out[w0] = acc;
+            } else {
+              atomicOr(p.out + w0, acc << o);
+              atomicOr(p.out + w0 + 1, acc >> (32 - o));
+            }
+          }
           acc = 0;
+          nb = 0;
         }
-        acc |= ((P >> k) & 1u) << (ob & 31);
       }
-      P = (P & ~(1u << k)) | (d << k);
-      if (k == 0) {
-        P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the block relayout
-        k = LB - 1;
-      } else {
-        --k;
-      }
+      if (tb0 >= sub_lo) P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the block relayout
+      t = tb0 - 1;
     }
-    if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+    if (nb > 0 && valid) {
+      const std::int64_t ol = obase + sub_lo;
+      const std::int64_t w0 = ol >> 5;
+      const int o = static_cast<int>(ol & 31);
+      atomicOr(p.out + w0, acc << o);
+      if (o + nb > 32) atomicOr(p.out + w0 + 1, acc >> (32 - o));
+    }
   }
 }
 
@@ -435,7 +533,7 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   // also the llr window must start at or before the first interior frame's beg
   if (p.llr_stage0 > fp.mi0 * p.f - p.v1) return false;
   fp.warps_per_cta = kWarpsPerCta;  // refined below from the shared-memory footprint
-  const int dec_bytes = (p.f + p.v2) * (R / 16 > 0 ? R / 16 : 1) * 32 * 4;
+  const int dec_bytes = (p.f + p.v2 + 1) * (R / 16 > 0 ? R / 16 : 1) * 32 * 4;  // + dummy row
   const int x_bytes = GEO::g > 0 ? GEO::GROUPS * GEO::XSTRIDE * 4 : 0;
   const int ss_bytes = ((GEO::FPW * fp.num_sub * 2) + 15) & ~15;
   fp.dec_off = 0;
