@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <type_traits>
 
 #include "vd_common.cuh"
 #include "vd_internal.h"
@@ -75,7 +76,55 @@ struct Geo {
   static constexpr int GROUPS = 32 / G;   // lane groups (frame pairs) per warp
   static constexpr int FPW = 2 * GROUPS;  // frames per warp
   static constexpr std::uint32_t SMASK = S - 1;
-  static constexpr int XSTRIDE = S + 4;   // relayout buffer words per group (bank padding)
+  // Relayout buffer: new-layout slot (lane', reg') at lane' * LSTRIDE + reg';
+  // the 4-word lane pitch and a group pitch = 20 (mod 32) words spread both
+  // the per-register STS.32 and the LDS.128 reads evenly over the banks.
+  struct Strides {
+    int l, x;
+  };
+  // Cost of one relayout: wavefronts of the LDS.128 reads (per quarter-warp,
+  // the max multiplicity of a 4-bank group) plus STS.32 conflict degree.
+  static constexpr int relayout_cost(int ls, int xs) {
+    int worst = 0;  // LDS.128 is serviced per quarter-warp: 8 lanes x 16 B
+    for (int h = 0; h < 4; ++h) {
+      int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+      for (int ln = 8 * h; ln < 8 * h + 8; ++ln) {
+        const int gq = ln / G, lm = ln % G;
+        cnt[((gq * xs + lm * ls) % 32) / 4] += 1;
+      }
+      int wq = 0;
+      for (int b = 0; b < 8; ++b) wq = cnt[b] > wq ? cnt[b] : wq;
+      worst += wq;
+    }
+    int sts = 0;
+    for (int i = 0; i < R; ++i) {
+      int bank[32] = {};
+      for (int ln = 0; ln < 32; ++ln) {
+        const int gq = ln / G, lm = ln % G;
+        const int pn = (i << g) | lm;
+        const int addr = gq * xs + (pn >> r) * ls + (pn & (R - 1));
+        bank[addr % 32] += 1;
+      }
+      for (int b = 0; b < 32; ++b) sts = bank[b] > sts ? bank[b] : sts;
+    }
+    return worst + sts;
+  }
+  static constexpr Strides pick_strides() {
+    Strides best{R, G * R};
+    int bc = 1 << 30;
+    for (int ls = R; ls < R + 32; ls += 4) {
+      for (int xs = G * ls; xs < G * ls + 32; xs += 4) {
+        const int c = relayout_cost(ls, xs) * 4096 + xs;  // prefer fewer conflicts, then less memory
+        if (c < bc) {
+          bc = c;
+          best = Strides{ls, xs};
+        }
+      }
+    }
+    return best;
+  }
+  static constexpr int LSTRIDE = pick_strides().l;
+  static constexpr int XSTRIDE = pick_strides().x;
   static_assert(R <= S && R >= 4 && (R & (R - 1)) == 0, "R must be a power of two in [4, S]");
   static_assert(G <= 32, "at most one frame pair per 32 lanes");
   static_assert(R % 4 == 0, "relayout reads use 128-bit loads");
@@ -113,8 +162,13 @@ struct FastParams {
   int nblk;               // blocks per frame (ceil(L / LB))
   int step, num_sub;      // subframe geometry
   int warps_per_cta;
-  int smem_per_warp;      // bytes
+  int smem_per_warp;      // bytes (per-warp area, after the CTA header)
   int dec_off, x_off, ss_off;  // byte offsets of the regions inside a warp's area
+  // Survivor store split: decisions of stages
+  // [t_first, t_split) live in tensor memory (tcols columns per warp, 32 TMEM
+  // lanes = the warp's lanes), stages [s_base, L) in shared memory rows
+  // (row = t - s_base); row smem_rows - 1 is a dummy sink.
+  int t_first, t_split, s_base, smem_rows, tcols;
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -122,6 +176,13 @@ struct FastParams {
 __device__ __forceinline__ std::uint32_t opaque(std::uint32_t x) {
   asm volatile("" : "+r"(x));
   return x;
+}
+// LLR prefetch load that the compiler may not sink towards its use (it would
+// otherwise trade the two-block prefetch distance for fewer live registers).
+__device__ __forceinline__ std::uint32_t ldg_pinned(const std::uint32_t* p) {
+  std::uint32_t v;
+  asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
 }
 
 // (a & m) | (b & ~m) as one LOP3 that the compiler cannot re-associate into a
@@ -152,21 +213,47 @@ struct FrameState {
   std::uint32_t sig[GEO::R];
   std::uint32_t wv[2][GEO::R];
   std::uint32_t fm[GEO::LB], k0[GEO::LB], k1[GEO::LB];  // per-lane LLR flip constants per phase
-  std::uint32_t cur[2][GEO::LB / 2];                     // LLR words of this block (frame A, B)
-  std::uint32_t nxt[2][GEO::LB / 2];                     // and of the next block
+  std::uint32_t llr[2][2][GEO::LB / 2];                  // [buffer][frame A/B][word]: even/odd blocks
 };
+
+// ---- tensor-memory survivor store --------------------------------------------
+__device__ __forceinline__ void tmem_st1(std::uint32_t taddr, std::uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void tmem_ld4(std::uint32_t taddr, std::uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr)
+               : "memory");
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
 
 struct BlockCtx {
   int v1, L;
-  std::uint32_t* drow_lane;  // dec + lane
+  std::uint32_t* drow_lane;  // smem survivor rows of this warp + lane
+  int s_base;                // stage of smem row 0
   int dummy_row;             // row index receiving out-of-range decision words
+  int t_first, t_split;      // TMEM holds stages [t_first, t_split)
+  std::uint32_t taddr;       // TMEM address of this warp's column t_first
 };
 
-// One block of LB stages. SLOW adds the per-stage range checks and the
-// stored-max argmax hook; FAST blocks (fully inside the stored range, no
-// argmax) are straight-line code.
-template <class C, class GEO, bool SLOW, class RecFn>
-__device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev, RecFn&& rec) {
+// Decision word of stage t -> its survivor slot (TMEM column or smem row).
+template <bool TM>
+__device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32_t word) {
+  const bool in = t >= bc.v1 && t < bc.L;
+  if (TM && in && t < bc.t_split) {
+    tmem_st1(bc.taddr + static_cast<std::uint32_t>(t - bc.t_first), word);
+  } else {
+    bc.drow_lane[(in ? t - bc.s_base : bc.dummy_row) * 32] = word;
+  }
+}
+
+// One block of LB stages. MODE 0 (slow) range-checks every pending store and
+// calls the stored-max argmax hook; MODE 1 / 2 are straight-line blocks whose
+// pending stores all go to shared memory / tensor memory.
+template <class C, class GEO, int MODE, bool TM, int BUF, class RecFn>
+__device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
+                                          const std::uint32_t* pfA, const std::uint32_t* pfB, RecFn&& rec) {
   constexpr int LB = GEO::LB, R = GEO::R;
   constexpr std::uint32_t BIAS = 0x80008000u;
   constexpr std::uint32_t OFF2 = 0x02000200u;
@@ -174,7 +261,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   std::uint32_t PT[LB][4], CL[LB][4];
 #pragma unroll
   for (int k = 0; k < LB; ++k) {
-    const std::uint32_t wA = st.cur[0][k >> 1], wB = st.cur[1][k >> 1];
+    const std::uint32_t wA = st.llr[BUF][0][k >> 1], wB = st.llr[BUF][1][k >> 1];
     const std::uint32_t o = (k & 1) * 2;
     const std::uint32_t sel = o | ((o + 1) << 4) | ((o + 4) << 8) | ((o + 5) << 12);
     const std::uint32_t tmp = prmt(wA, wB, sel) ^ st.fm[k];
@@ -186,6 +273,13 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     PT[k][2] = OFF2 - PT[k][1];                      // T2 = -T1
 #pragma unroll
     for (int x = 0; x < 4; ++x) CL[k][x] = PT[k][x ^ 3] - PT[k][x] + BIAS;
+  }
+  // The words of this buffer are consumed: refill it with block blk + 2 now,
+  // so two full blocks of work cover the HBM latency.
+#pragma unroll
+  for (int i = 0; i < LB / 2; ++i) {
+    st.llr[BUF][0][i] = ldg_pinned(pfA + i);
+    st.llr[BUF][1][i] = ldg_pinned(pfB + i);
   }
 #pragma unroll
   for (int k = 0; k < LB; ++k) {
@@ -205,27 +299,29 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       st.sig[e] = __viaddmax_s16x2(sE, PT[k][x], s2L);
       st.sig[od] = __viaddmax_s16x2(sE, PT[k][x ^ 3], s2H);
     }
-    // ---- previous stage's decisions -> shared memory (overlaps this ACS) ---
+    // ---- previous stage's decisions -> survivor store (overlaps this ACS) --
     const std::uint32_t word = compact16(st.wv[(k + 1) & 1]);
-    if constexpr (SLOW) {
-      const int row = (tprev >= bc.v1 && tprev < bc.L) ? tprev - bc.v1 : bc.dummy_row;
-      bc.drow_lane[row * 32] = word;
+    if constexpr (MODE == 0) {
+      store_dec<TM>(bc, tprev, word);
       tprev = t;
       rec(t, k);
+    } else if constexpr (MODE == 1) {
+      bc.drow_lane[(t - 1 - bc.s_base) * 32] = word;
     } else {
-      bc.drow_lane[(t - 1 - bc.v1) * 32] = word;
+      tmem_st1(bc.taddr + static_cast<std::uint32_t>(t - 1 - bc.t_first), word);
     }
   }
-  if constexpr (!SLOW) tprev = blk * LB + LB - 1;
+  if constexpr (MODE != 0) tprev = blk * LB + LB - 1;
 }
 
-template <class C, int R>
-__global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
+template <class C, int R, bool TM>
+__global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   using GEO = Geo<C, R>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, r = GEO::r, g = GEO::g;
   constexpr std::uint32_t BASE = 0x20002000u;  // offset-binary metric origin (8192 per half)
   constexpr int WPB = LB / 2;
   static_assert(LB % 2 == 0, "B=2 fast path needs an even block length");
+  static_assert(LB == 4, "tensor-memory blocks are 4 columns");
   static_assert(R == 16, "one 32-bit decision word per lane per stage");
   const DecodeLaunch& p = fp.p;
 
@@ -234,19 +330,43 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
   const int warp = threadIdx.x >> 5;
   const int grp = lane / G;
   const int lam = lane % G;
-  unsigned char* wbase = smem_raw + static_cast<std::size_t>(warp) * fp.smem_per_warp;
+  std::uint32_t* tmem_slot = reinterpret_cast<std::uint32_t*>(smem_raw);  // CTA header (16 B)
+  unsigned char* wbase = smem_raw + 16 + static_cast<std::size_t>(warp) * fp.smem_per_warp;
   std::uint32_t* dec = reinterpret_cast<std::uint32_t*>(wbase + fp.dec_off);
   std::uint32_t* xbuf = reinterpret_cast<std::uint32_t*>(wbase + fp.x_off);
   std::uint16_t* sstate = reinterpret_cast<std::uint16_t*>(wbase + fp.ss_off);
 
+  // ---- tensor-memory allocation (one warp allocates for the CTA) ------------
+  std::uint32_t tbase = 0;
+  if constexpr (TM) {
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+          static_cast<unsigned>(__cvta_generic_to_shared(tmem_slot))));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    tbase = *tmem_slot;
+  }
+
   const std::int64_t gwarp = static_cast<std::int64_t>(blockIdx.x) * fp.warps_per_cta + warp;
   const std::int64_t mbase = fp.mi0 + gwarp * GEO::FPW;
-  if (mbase >= fp.mi1) return;  // whole warp idle (uniform)
+  if (mbase < fp.mi1) {  // (no early return: TMEM dealloc needs every warp at the barrier)
   const std::int64_t mA = mbase + 2 * grp, mB = mA + 1;
   const bool validA = mA < fp.mi1, validB = mB < fp.mi1;
   const std::int64_t lA = validA ? mA : fp.mi0, lB = validB ? mB : fp.mi0;  // clamp loads
 
-  const int f = p.f, v1 = p.v1, v2 = p.v2, L = fp.L;
+  const int f = static_cast<int>(opaque(static_cast<std::uint32_t>(p.f)));
+  const int v1 = static_cast<int>(opaque(static_cast<std::uint32_t>(p.v1)));
+  const int v2 = static_cast<int>(opaque(static_cast<std::uint32_t>(p.v2)));
+  const int L = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.L)));
+  const int nblk = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.nblk)));
+  const int num_sub = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.num_sub)));
+  const int step = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.step)));
+  const int t_split = TM ? static_cast<int>(opaque(static_cast<std::uint32_t>(fp.t_split))) : v1;
+  const int t_first = TM ? static_cast<int>(opaque(static_cast<std::uint32_t>(fp.t_first))) : v1;
+  const int s_base = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.s_base)));
   // Frame-relative LLR word pointers (frame start is 4-byte aligned: checked at launch).
   const std::uint32_t* llrA = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
                                                                      (lA * f - v1 - p.llr_stage0) * 2);
@@ -274,24 +394,27 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
   std::int32_t subA = 0, subB = 0;  // accumulated renormalisation (ref - BASE) per half
 
 #pragma unroll
-  for (int i = 0; i < WPB; ++i) {
-    st.cur[0][i] = __ldg(llrA + i);
-    st.cur[1][i] = __ldg(llrB + i);
-    st.nxt[0][i] = __ldg(llrA + WPB + i);
-    st.nxt[1][i] = __ldg(llrB + WPB + i);
+  for (int b = 0; b < 2; ++b) {
+#pragma unroll
+    for (int i = 0; i < WPB; ++i) {
+      st.llr[b][0][i] = __ldg(llrA + b * WPB + i);
+      st.llr[b][1][i] = __ldg(llrB + b * WPB + i);
+    }
   }
+  // Prefetch pointers: block b + 2 is requested right after block b has
+  // built its tables (two blocks of latency cover).
   const std::uint32_t* pfA = llrA + 2 * WPB;
   const std::uint32_t* pfB = llrB + 2 * WPB;
 
   int next_sub = 0;
   // subframes whose traceback starts from the stored max state
-  auto sub_start = [&](int s) { return v1 + min((s + 1) * fp.step, f) + v2 - 1; };
+  auto sub_start = [&](int s) { return v1 + min((s + 1) * step, f) + v2 - 1; };
   auto needs_record = [&](int s) {
     const int sst = sub_start(s);
     return !(p.f0 > 0 && p.start == 1 && sst < L - 1);
   };
-  while (next_sub < fp.num_sub && !needs_record(next_sub)) ++next_sub;
-  int next_rec = next_sub < fp.num_sub ? sub_start(next_sub) : 0x7fffffff;
+  while (next_sub < num_sub && !needs_record(next_sub)) ++next_sub;
+  int next_rec = next_sub < num_sub ? sub_start(next_sub) : 0x7fffffff;
 
   // stored-max argmax at start stages (decoder.cpp:205-211)
   auto rec = [&](int t, int k) {
@@ -315,8 +438,8 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
       bestB = max(bestB, __shfl_xor_sync(kFull, bestB, o2));
     }
     if (lam == 0) {
-      sstate[(2 * grp) * fp.num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestA & 0xffffu));
-      sstate[(2 * grp + 1) * fp.num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestB & 0xffffu));
+      sstate[(2 * grp) * num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestA & 0xffffu));
+      sstate[(2 * grp + 1) * num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestB & 0xffffu));
     }
     if (t == L - 1 && p.sigma != nullptr) {
       // final metrics: true = stored - BASE - 256 * L + sum(ref - BASE)
@@ -331,37 +454,26 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
       }
     }
     ++next_sub;
-    while (next_sub < fp.num_sub && !needs_record(next_sub)) ++next_sub;
-    next_rec = next_sub < fp.num_sub ? sub_start(next_sub) : 0x7fffffff;
+    while (next_sub < num_sub && !needs_record(next_sub)) ++next_sub;
+    next_rec = next_sub < num_sub ? sub_start(next_sub) : 0x7fffffff;
   };
 
   BlockCtx bc;
   bc.v1 = v1;
   bc.L = L;
   bc.drow_lane = dec + lane;
-  bc.dummy_row = f + v2;  // one spare row after the stored range
+  bc.s_base = s_base;
+  bc.dummy_row = fp.smem_rows - 1;
+  bc.t_first = t_first;
+  bc.t_split = t_split;
+  // this warp's TMEM lanes (32 * (warp % 4)) and columns (tcols * (warp / 4))
+  bc.taddr = tbase + ((32u * static_cast<std::uint32_t>(warp & 3)) << 16) +
+             static_cast<std::uint32_t>(fp.tcols * (warp >> 2));
   int tprev = -1;
 
-  for (int blk = 0; blk < fp.nblk; ++blk) {
-    const int t0 = blk * LB;
-    // fast block: every pending store (stages t0-1 .. t0+LB-2) is in range and
-    // no start stage falls inside the block
-    const bool fast = (t0 - 1 >= v1) && (t0 + LB - 2 < L) && !(next_rec >= t0 && next_rec < t0 + LB);
-    if (fast) {
-      run_block<C, GEO, false>(st, blk, bc, tprev, rec);
-    } else {
-      run_block<C, GEO, true>(st, blk, bc, tprev, rec);
-    }
-    // ---- LLR pipeline: advance one block, prefetch the block after next ----
-#pragma unroll
-    for (int i = 0; i < WPB; ++i) {
-      st.cur[0][i] = st.nxt[0][i];
-      st.cur[1][i] = st.nxt[1][i];
-      st.nxt[0][i] = __ldg(pfA + i);
-      st.nxt[1][i] = __ldg(pfB + i);
-    }
-    pfA += WPB;
-    pfB += WPB;
+  // (opaque offset, not pointer: the accesses must stay STS/LDS)
+  std::uint32_t* const xb = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE));
+  auto block_end = [&](int blk) {
     // ---- renormalisation every 2 blocks (group-wide reference) ------------
     if (blk & 1) {
       const std::uint32_t ref = __shfl_sync(kFull, st.sig[0], grp * G);
@@ -372,11 +484,15 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
     }
     // ---- relayout: back to the canonical layout (P_new = rotr(P_old, r)) --
     if constexpr (g > 0) {
-      std::uint32_t* xb = xbuf + grp * GEO::XSTRIDE;
 #pragma unroll
-      for (int i = 0; i < R; ++i) xb[(i << g) | lam] = st.sig[i];
+      for (int i = 0; i < R; ++i) {
+        // old (lam, i) -> new physical index rotr(lam * R + i, r) = (i << g) | lam
+        const int pn_reg = ((i << g) & (R - 1));  // compile-time part of the new register index
+        const int pn_lane = (i << g) >> r;        // compile-time part of the new lane index
+        xb[(pn_lane + (lam >> r)) * GEO::LSTRIDE + pn_reg + (lam & (R - 1))] = st.sig[i];
+      }
       __syncwarp();
-      const uint4* src = reinterpret_cast<const uint4*>(xb + lam * R);
+      const uint4* src = reinterpret_cast<const uint4*>(xb + lam * GEO::LSTRIDE);
 #pragma unroll
       for (int i = 0; i < R / 4; ++i) {
         const uint4 v = src[i];
@@ -387,96 +503,137 @@ __global__ void __launch_bounds__(256) fast_kernel(const FastParams fp) {
       }
       __syncwarp();
     }
+  };
+  auto one_block = [&](int blk, auto buf_tag) {
+    constexpr int BUF = decltype(buf_tag)::value;
+    const int t0 = blk * LB;
+    // Straight-line block: pending stores (stages t0-1 .. t0+LB-2) all inside
+    // [v1, L) and on one side of the TMEM/smem split, no start stage inside.
+    const bool clean = (t0 - 1 >= v1) && (t0 + LB - 2 < L) && !(next_rec >= t0 && next_rec < t0 + LB);
+    if (clean && t0 - 1 >= t_split) {
+      run_block<C, GEO, 1, TM, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
+    } else if (TM && clean && t0 + LB - 2 < t_split) {
+      run_block<C, GEO, 2, TM, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
+    } else {
+      run_block<C, GEO, 0, TM, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
+    }
+    pfA += WPB;
+    pfB += WPB;
+    block_end(blk);
+  };
+  for (int blk = 0; blk < nblk; blk += 2) {
+    one_block(blk, std::integral_constant<int, 0>{});
+    if (blk + 1 < nblk) one_block(blk + 1, std::integral_constant<int, 1>{});
   }
   // decisions of the last processed stage
-  {
-    const std::uint32_t word = compact16(st.wv[(fp.nblk * LB - 1) & 1]);
-    const int row = (tprev >= v1 && tprev < L) ? tprev - v1 : bc.dummy_row;
-    bc.drow_lane[row * 32] = word;
-  }
+  store_dec<TM>(bc, tprev, compact16(st.wv[(nblk * LB - 1) & 1]));
+  if constexpr (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   __syncwarp();
 
   // ---- subframe-parallel traceback (decoder.cpp:214-236) --------------------
   // Tasks (frame, subframe) are spread over all 32 lanes of the warp, frames
-  // fastest: in a round every lane traces one task, reading any group's
-  // decision words from shared memory. Within a block of LB stages the lane
-  // index of the traced state (P >> r) is fixed (only register bits are
-  // rewritten), so the block's words are fetched together: one shared-memory
-  // latency per LB steps, and the per-step work is branch-free.
-  const int ntask = GEO::FPW * fp.num_sub;
-  for (int task = lane; task - lane < ntask; task += 32) {
+  // fastest; the block loop is warp-uniform (the union of the round's task
+  // ranges) so tensor-memory loads, which are warp-collective, can be used.
+  // Within a block of LB stages the lane index of a traced state (P >> r) is
+  // fixed (only register bits are rewritten): the block's 4 words come from
+  // one TMEM load + shuffles or 4 independent LDS, then the per-step work is
+  // branch-free. Output bit of phase j = bit j of P at block entry.
+  const int ntask = GEO::FPW * num_sub;
+  for (int base = 0; base < ntask; base += 32) {
+    const int task = base + lane;
     const bool active = task < ntask;
     const int fr = active ? task % GEO::FPW : 0;  // frame slot in the warp (2 * group + half)
     const int s = active ? task / GEO::FPW : 0;
     const int half = fr & 1;
     const std::int64_t m = mbase + fr;
     const bool valid = active && m < fp.mi1;
-    const int st = sub_start(s);
-    const int sub_lo = v1 + s * fp.step;
-    const int sub_hi = v1 + min((s + 1) * fp.step, f);
+    const int st_t = active ? sub_start(s) : -1;
+    const int sub_lo = v1 + s * step;
+    const int sub_hi = v1 + min((s + 1) * step, f);
     std::uint32_t state;
-    if (p.f0 > 0 && p.start == 1 && st < L - 1) {
+    if (p.f0 > 0 && p.start == 1 && st_t < L - 1) {
       state = static_cast<std::uint32_t>(mix_seed(p.seed, static_cast<std::uint64_t>(m) * 0x10001ull +
                                                               static_cast<std::uint64_t>(s)) %
                                          static_cast<std::uint64_t>(S));
     } else {
-      state = sstate[fr * fp.num_sub + s];
+      state = sstate[fr * num_sub + s];
     }
     // physical index after stage st (phase st % LB): rotl(state, phase + 1)
-    const int sh = ((st & (LB - 1)) + 1) % M;
+    const int sh = ((st_t & (LB - 1)) + 1) % M;
     std::uint32_t P = sh == 0 ? state : (((state << sh) | (state >> (M - sh))) & GEO::SMASK);
     const std::uint32_t hsh = half ? 16u : 0u;
-    const std::uint32_t* gdec = dec + (fr >> 1) * G;  // this frame's group columns
+    const int gcol = (fr >> 1) * G;  // this frame's group: first lane of its decision columns
     const std::int64_t obase = m * f - v1 - p.out_stage0;  // output bit index of frame-relative stage 0
-    std::uint32_t acc = 0;
+    std::uint64_t acc = 0;  // emitted bits, newest (lowest stage) at bit 0
     int nb = 0;
-    int t = st;
-    while (t >= sub_lo) {
-      const int tb0 = t & ~(LB - 1);
+    const int thi = __reduce_max_sync(kFull, static_cast<unsigned>(st_t + 1)) - 1;
+    const int tlo = static_cast<int>(__reduce_min_sync(kFull, active ? static_cast<unsigned>(sub_lo) : 0x7fffffffu));
+    for (int tb0 = thi & ~(LB - 1); tb0 >= (tlo & ~(LB - 1)); tb0 -= LB) {
       const std::uint32_t lp = P >> r;
       std::uint32_t wd[LB];
+      if (TM && tb0 < t_split) {
+        std::uint32_t own[4];
+        tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
 #pragma unroll
-      for (int j = 0; j < LB; ++j) {
-        const int row = max(tb0 + j - v1, 0);
-        wd[j] = gdec[row * 32 + lp];
+        for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
+      } else {
+#pragma unroll
+        for (int j = 0; j < LB; ++j) {
+          const int row = max(tb0 + j - s_base, 0);
+          wd[j] = dec[row * 32 + gcol + lp];
+        }
       }
+      const int jhi = st_t - tb0;                       // phases jlo..jhi of this block are walked
+      const int jlo = sub_lo > tb0 ? sub_lo - tb0 : 0;
+      const int ehi = min(jhi, sub_hi - 1 - tb0);
+      const std::uint32_t Pin = P;
+      std::uint32_t u = P & (R - 1);
 #pragma unroll
       for (int j = LB - 1; j >= 0; --j) {
-        const int sj = tb0 + j;
-        const bool in = sj <= t && sj >= sub_lo;
-        const std::uint32_t dbit = (wd[j] >> ((P & (R - 1)) | hsh)) & 1u;
-        const bool em = in && sj < sub_hi;
-        const std::uint32_t ob = (P >> j) & 1u;
-        acc = em ? ((acc << 1) | ob) : acc;
-        nb += em ? 1 : 0;
-        const std::uint32_t Pn = (P & ~(1u << j)) | (dbit << j);
-        P = in ? Pn : P;
-        if (nb == 32) {
-          const std::int64_t ol = obase + sj;  // lowest output index held in acc
+        const std::uint32_t dbit = (wd[j] >> (u | hsh)) & 1u;
+        const std::uint32_t un = (u & ~(1u << j)) | (dbit << j);
+        u = (j <= jhi && j >= jlo) ? un : u;
+      }
+      P = (P & ~static_cast<std::uint32_t>(R - 1)) | u;
+      const int ejhi = min(ehi, LB - 1);
+      if (ejhi >= jlo) {
+        const int n = ejhi - jlo + 1;
+        acc = (acc << n) | ((Pin >> jlo) & ((1u << n) - 1u));
+        nb += n;
+        if (nb >= 32) {
+          // the oldest 32 bits: stages tb0 + jlo + (nb - 32) ... + 31
+          const std::uint32_t word = static_cast<std::uint32_t>(acc >> (nb - 32));
+          const std::int64_t ol = obase + tb0 + jlo + (nb - 32);
           const std::int64_t w0 = ol >> 5;
           const int o = static_cast<int>(ol & 31);
           if (valid) {
             if (o == 0) {
-              p.out[w0] = acc;
+              p.out[w0] = word;
             } else {
-              atomicOr(p.out + w0, acc << o);
-              atomicOr(p.out + w0 + 1, acc >> (32 - o));
+              atomicOr(p.out + w0, word << o);
+              atomicOr(p.out + w0 + 1, word >> (32 - o));
             }
           }
-          acc = 0;
-          nb = 0;
+          nb -= 32;
         }
       }
-      if (tb0 >= sub_lo) P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the block relayout
-      t = tb0 - 1;
+      if (tb0 >= sub_lo && tb0 <= st_t) P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the relayout
     }
     if (nb > 0 && valid) {
+      const std::uint32_t word = static_cast<std::uint32_t>(acc) & ((nb == 32) ? 0xffffffffu : ((1u << nb) - 1u));
       const std::int64_t ol = obase + sub_lo;
       const std::int64_t w0 = ol >> 5;
       const int o = static_cast<int>(ol & 31);
-      atomicOr(p.out + w0, acc << o);
-      if (o + nb > 32) atomicOr(p.out + w0 + 1, acc >> (32 - o));
+      atomicOr(p.out + w0, word << o);
+      if (o + nb > 32) atomicOr(p.out + w0 + 1, word >> (32 - o));
     }
+  }
+  }  // mbase < mi1
+
+  if constexpr (TM) {
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
   }
 }
 
@@ -498,13 +655,15 @@ using K8a = Code2<8, 0247, 0371>;
 static_assert(K7a::sym() && K7b::sym() && K9a::sym() && K9b::sym() && K5a::sym() && K6a::sym() && K8a::sym(),
               "fast-path codes must tap the newest and oldest register bits");
 
-constexpr int kWarpsPerCta = 4;
-constexpr int kMaxWarpsPerCta = 8;
-constexpr int kSmemMax = 232448;  // sm_100 max dynamic shared memory per CTA
+constexpr int kMaxWarpsSmem = 8;   // smem-only survivor store
+constexpr int kWarpsTmem = 12;     // TMEM + smem survivor store: 3 warps per TMEM lane quarter
+constexpr int kSmemMax = 232448;   // sm_100 max dynamic shared memory per CTA
+constexpr int kHeader = 16;        // CTA header: TMEM base address
 
 struct Plan {
   FastParams fp;
   std::size_t smem;
+  bool tm;
 };
 
 template <class C, int R>
@@ -532,21 +691,38 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   if (fp.mi1 - fp.mi0 < GEO::FPW) return false;  // not worth it
   // also the llr window must start at or before the first interior frame's beg
   if (p.llr_stage0 > fp.mi0 * p.f - p.v1) return false;
-  fp.warps_per_cta = kWarpsPerCta;  // refined below from the shared-memory footprint
-  const int dec_bytes = (p.f + p.v2 + 1) * (R / 16 > 0 ? R / 16 : 1) * 32 * 4;  // + dummy row
   const int x_bytes = GEO::g > 0 ? GEO::GROUPS * GEO::XSTRIDE * 4 : 0;
   const int ss_bytes = ((GEO::FPW * fp.num_sub * 2) + 15) & ~15;
-  fp.dec_off = 0;
-  fp.x_off = dec_bytes;
-  fp.ss_off = dec_bytes + x_bytes;
-  fp.smem_per_warp = (dec_bytes + x_bytes + ss_bytes + 15) & ~15;
-  // As many warps per CTA as fit in the 227 KB opt-in shared memory (one CTA
-  // per SM when the decision store is large), at most 8.
-  int w = kSmemMax / fp.smem_per_warp;
-  if (w < 1) return false;
-  fp.warps_per_cta = w < kMaxWarpsPerCta ? w : kMaxWarpsPerCta;
+  auto layout = [&](int smem_rows) {
+    const int dec_bytes = smem_rows * 32 * 4;
+    fp.smem_rows = smem_rows;
+    fp.dec_off = 0;
+    fp.x_off = dec_bytes;
+    fp.ss_off = dec_bytes + x_bytes;
+    fp.smem_per_warp = (dec_bytes + x_bytes + ss_bytes + 15) & ~15;
+  };
+  // Preferred: 12 warps per CTA (3 per SMSP), survivors split between tensor
+  // memory (168 columns per warp) and shared memory.
+  fp.tcols = ((512 / (kWarpsTmem / 4)) & ~3);
+  fp.t_first = p.v1 & ~3;
+  fp.t_split = fp.t_first + fp.tcols;
+  fp.s_base = fp.t_split;
+  layout(std::max(fp.L - fp.t_split, 0) + 1);
+  if (kHeader + static_cast<std::size_t>(fp.smem_per_warp) * kWarpsTmem <= static_cast<std::size_t>(kSmemMax)) {
+    fp.warps_per_cta = kWarpsTmem;
+    out->tm = true;
+  } else {
+    // Long frames: shared memory only, as many warps as fit.
+    fp.tcols = 0;
+    fp.t_first = fp.t_split = fp.s_base = p.v1;
+    layout(p.f + p.v2 + 1);
+    const int w = (kSmemMax - kHeader) / fp.smem_per_warp;
+    if (w < 1) return false;
+    fp.warps_per_cta = std::min(w, kMaxWarpsSmem);
+    out->tm = false;
+  }
   out->fp = fp;
-  out->smem = static_cast<std::size_t>(fp.smem_per_warp) * fp.warps_per_cta;
+  out->smem = kHeader + static_cast<std::size_t>(fp.smem_per_warp) * fp.warps_per_cta;
   return true;
 }
 
@@ -568,12 +744,9 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
     if (p.sigma) e.sigma = static_cast<std::int64_t*>(p.sigma) + (fp.mi1 - p.frame_begin) * p.s;
     if (cudaError_t err = launch_generic_i8(e, stream); err != cudaSuccess) return err;
   }
-  if (p.sigma && fp.mi0 > p.frame_begin) {
-    // the head launch above wrote sigma for frames [frame_begin, mi0) at offset 0 (correct)
-  }
   const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
   const std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
-  auto kern = fast_kernel<C, R>;
+  auto kern = pl.tm ? fast_kernel<C, R, true> : fast_kernel<C, R, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem));
   if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fp);
