@@ -19,8 +19,8 @@
 //    keep every stage inside a lane for LB = log2(R) stages; one shared-memory
 //    relayout (STS.32 x R + LDS.128 x R/4 per lane) then restores the
 //    canonical layout, so the code for a block of LB stages repeats forever.
-//  * Path metrics are offset-binary int16 (kept in [~4k, ~16k] by a group-wide
-//    renormalisation every 2 blocks), which lets one 32-bit IADD3 produce both
+//  * Path metrics are offset-binary int16 (kept in [~4k, ~21k] by a group-wide
+//    renormalisation every 4 blocks), which lets one 32-bit IADD3 produce both
 //    halves' decision bits: w = sigma_O - sigma_E + C has bit 15 / 31 set iff
 //    the second predecessor wins, ties included (reference decoder.cpp:67-74).
 //  * Decision bits are gathered with PRMT sign-replication + LOP3 merges into
@@ -474,8 +474,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   // (opaque offset, not pointer: the accesses must stay STS/LDS)
   std::uint32_t* const xb = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE));
   auto block_end = [&](int blk) {
-    // ---- renormalisation every 2 blocks (group-wide reference) ------------
-    if (blk & 1) {
+    // ---- renormalisation every 4 blocks (group-wide reference): metrics stay
+    // within [BASE - spread, BASE + spread + 16 * 510] (< 32768 up to K = 9).
+    if ((blk & 3) == 3) {
       const std::uint32_t ref = __shfl_sync(kFull, st.sig[0], grp * G);
       subA += static_cast<std::int32_t>(ref & 0xffffu) - 8192;
       subB += static_cast<std::int32_t>(ref >> 16) - 8192;
@@ -566,8 +567,33 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     const std::int64_t obase = m * f - v1 - p.out_stage0;  // output bit index of frame-relative stage 0
     std::uint64_t acc = 0;  // emitted bits, newest (lowest stage) at bit 0
     int nb = 0;
-    const int thi = __reduce_max_sync(kFull, static_cast<unsigned>(st_t + 1)) - 1;
+    // Round-uniform bounds (inactive lanes have st_t = -1 and sub_lo = v1).
+    const int thi = static_cast<int>(__reduce_max_sync(kFull, static_cast<unsigned>(st_t + 1))) - 1;
     const int tlo = static_cast<int>(__reduce_min_sync(kFull, active ? static_cast<unsigned>(sub_lo) : 0x7fffffffu));
+    const int st_min = static_cast<int>(__reduce_min_sync(kFull, active ? static_cast<unsigned>(st_t) : 0x7fffffffu));
+    const int lo_max = static_cast<int>(__reduce_max_sync(kFull, active ? static_cast<unsigned>(sub_lo) : 0u));
+    const int hi_min = static_cast<int>(__reduce_min_sync(kFull, active ? static_cast<unsigned>(sub_hi) : 0x7fffffffu));
+    const int hi_max = static_cast<int>(__reduce_max_sync(kFull, active ? static_cast<unsigned>(sub_hi) : 0u));
+    auto emit = [&](int tb0, int jlo, int n, std::uint32_t bits) {
+      acc = (acc << n) | bits;
+      nb += n;
+      if (nb >= 32) {
+        // the oldest 32 bits: stages tb0 + jlo + (nb - 32) ... + 31
+        const std::uint32_t word = static_cast<std::uint32_t>(acc >> (nb - 32));
+        const std::int64_t ol = obase + tb0 + jlo + (nb - 32);
+        const std::int64_t w0 = ol >> 5;
+        const int o = static_cast<int>(ol & 31);
+        if (valid) {
+          if (o == 0) {
+            p.out[w0] = word;
+          } else {
+            atomicOr(p.out + w0, word << o);
+            atomicOr(p.out + w0 + 1, word >> (32 - o));
+          }
+        }
+        nb -= 32;
+      }
+    };
     for (int tb0 = thi & ~(LB - 1); tb0 >= (tlo & ~(LB - 1)); tb0 -= LB) {
       const std::uint32_t lp = P >> r;
       std::uint32_t wd[LB];
@@ -575,49 +601,45 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
         std::uint32_t own[4];
         tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
 #pragma unroll
-        for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
+        for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp)) >> hsh;
       } else {
 #pragma unroll
         for (int j = 0; j < LB; ++j) {
           const int row = max(tb0 + j - s_base, 0);
-          wd[j] = dec[row * 32 + gcol + lp];
+          wd[j] = dec[row * 32 + gcol + lp] >> hsh;
         }
       }
-      const int jhi = st_t - tb0;                       // phases jlo..jhi of this block are walked
-      const int jlo = sub_lo > tb0 ? sub_lo - tb0 : 0;
-      const int ehi = min(jhi, sub_hi - 1 - tb0);
       const std::uint32_t Pin = P;
       std::uint32_t u = P & (R - 1);
+      if (tb0 + LB - 1 <= st_min && tb0 >= lo_max) {
+        // every task walks all LB phases of this block
 #pragma unroll
-      for (int j = LB - 1; j >= 0; --j) {
-        const std::uint32_t dbit = (wd[j] >> (u | hsh)) & 1u;
-        const std::uint32_t un = (u & ~(1u << j)) | (dbit << j);
-        u = (j <= jhi && j >= jlo) ? un : u;
-      }
-      P = (P & ~static_cast<std::uint32_t>(R - 1)) | u;
-      const int ejhi = min(ehi, LB - 1);
-      if (ejhi >= jlo) {
-        const int n = ejhi - jlo + 1;
-        acc = (acc << n) | ((Pin >> jlo) & ((1u << n) - 1u));
-        nb += n;
-        if (nb >= 32) {
-          // the oldest 32 bits: stages tb0 + jlo + (nb - 32) ... + 31
-          const std::uint32_t word = static_cast<std::uint32_t>(acc >> (nb - 32));
-          const std::int64_t ol = obase + tb0 + jlo + (nb - 32);
-          const std::int64_t w0 = ol >> 5;
-          const int o = static_cast<int>(ol & 31);
-          if (valid) {
-            if (o == 0) {
-              p.out[w0] = word;
-            } else {
-              atomicOr(p.out + w0, word << o);
-              atomicOr(p.out + w0 + 1, word >> (32 - o));
-            }
-          }
-          nb -= 32;
+        for (int j = LB - 1; j >= 0; --j) {
+          const std::uint32_t dbit = (wd[j] >> u) & 1u;
+          u = (u & ~(1u << j)) | (dbit << j);
         }
+        P = (P & ~static_cast<std::uint32_t>(R - 1)) | u;
+        if (tb0 + LB - 1 < hi_min) {
+          emit(tb0, 0, LB, Pin & ((1u << LB) - 1u));
+        } else if (tb0 < hi_max) {
+          const int ejhi = min(sub_hi - 1 - tb0, LB - 1);
+          if (ejhi >= 0) emit(tb0, 0, ejhi + 1, Pin & ((1u << (ejhi + 1)) - 1u));
+        }
+        P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the block relayout
+      } else {
+        const int jhi = st_t - tb0;  // phases jlo..jhi of this block are walked
+        const int jlo = sub_lo > tb0 ? sub_lo - tb0 : 0;
+#pragma unroll
+        for (int j = LB - 1; j >= 0; --j) {
+          const std::uint32_t dbit = (wd[j] >> u) & 1u;
+          const std::uint32_t un = (u & ~(1u << j)) | (dbit << j);
+          u = (j <= jhi && j >= jlo) ? un : u;
+        }
+        P = (P & ~static_cast<std::uint32_t>(R - 1)) | u;
+        const int ejhi = min(min(jhi, sub_hi - 1 - tb0), LB - 1);
+        if (ejhi >= jlo) emit(tb0, jlo, ejhi - jlo + 1, (Pin >> jlo) & ((1u << (ejhi - jlo + 1)) - 1u));
+        if (tb0 >= sub_lo && tb0 <= st_t) P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the relayout
       }
-      if (tb0 >= sub_lo && tb0 <= st_t) P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the relayout
     }
     if (nb > 0 && valid) {
       const std::uint32_t word = static_cast<std::uint32_t>(acc) & ((nb == 32) ? 0xffffffffu : ((1u << nb) - 1u));
