@@ -44,7 +44,7 @@ EBN0 = 3.0
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--stages", type=int, default=1 << 32, help="info bits per rank per step")
@@ -284,16 +284,18 @@ def run_ours(args):
     same = bool(torch.equal(host_out[:words], out[:words].cpu()))
 
     # ---- roofline ----------------------------------------------------------
+    # Binding roof: integer ALU. The packed ACS (VIADD.16x2 on the fmaheavy
+    # pipe + VIADDMNMX.S16x2 on the alu pipe, each 0.5 warp-instr/clk/SMSP as
+    # measured with ncu in profiles/r01_pipe_probe_ncu.csv) retires 2 states x
+    # 3 ops per instruction pair: 4 SMSP x 32 lanes x 0.5 x 6 = 384 lane-ops
+    # per SM clock. HBM roof reported alongside.
     peaks, peak_src = measured_peaks()
-    alu_peak = None
-    alu_src = None
-    mb = ROOT / "profiles" / "alu_peak.json"
-    if mb.exists():
-        d = json.loads(mb.read_text())
-        alu_peak, alu_src = d.get("tops"), d.get("source", "microbenchmark")
-    if alu_peak is None:
-        alu_peak = 148 * 128 * peaks.get("sm_max_mhz", 1965.0) * 1e6 / 1e12
-        alu_src = "theoretical 148 SM x 64 lanes x 2 (packed 16x2) x max clock"
+    clocks = clk.summary()
+    sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
+    sms = torch.cuda.get_device_properties(dev).multi_processor_count
+    alu_peak = sms * 384 * sm_mhz * 1e6 / 1e12
+    alu_src = (f"{sms} SM x 384 packed-ACS lane-ops/clk (ncu-measured pipe rates, profiles/r01_pipe_probe_ncu.csv) "
+               f"x {sm_mhz:.0f} MHz (median SM clock during the timed region)")
     ops_bit = alu_ops_per_bit(stats.stages, n)
     bits_per_s_kernel = n / (ms_step * 1e-3)
     alu_achieved = ops_bit * bits_per_s_kernel / 1e12
@@ -302,7 +304,7 @@ def run_ours(args):
     traffic = None
     tp = ROOT / "profiles" / "decode_traffic.json"
     if tp.exists():
-        traffic = json.loads(tp.read_text()).get("bytes_per_launch")
+        traffic = json.loads(tp.read_text()).get("bytes_per_bit", 0) * n
 
     result = None
     if rank == 0:
@@ -310,7 +312,6 @@ def run_ours(args):
         if not args.no_cpu:
             g, cores, kind, sample, _ = cpu_reference_rate(args.cpu_seconds)
             cpu = {"value": g, "unit": "Gbps", "cores": cores, "kind": kind, "sample": sample}
-        clocks = clk.summary()
         result = {
             "metric": "decoded info Gbps (K=7 r1/2 soft)",
             "value": gbps,
@@ -350,7 +351,7 @@ def run_ours(args):
             "e2e": {"value": e2e_gbps, "unit": "Gbps", "h2d_bytes_per_step": ne * 2,
                     "d2h_bytes_per_step": ((ne + 31) // 32) * 4, "info_bits_per_step": ne,
                     "matches_device_decode": same},
-            "gpu_launches": args.steps,
+            "gpu_launches": 3 * args.steps,  # per step: head/tail edge frames (generic) + fast kernel
             "clocks": clocks,
         }
         print(json.dumps(result))
