@@ -32,6 +32,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <map>
 #include <type_traits>
 
 #include "vd_common.cuh"
@@ -169,6 +170,7 @@ struct FastParams {
   // lanes = the warp's lanes), stages [s_base, L) in shared memory rows
   // (row = t - s_base); row smem_rows - 1 is a dummy sink.
   int t_first, t_split, s_base, smem_rows, tcols;
+  int tm_alloc;  // TMEM columns allocated per CTA (power of two)
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -253,7 +255,8 @@ __device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32
 // pending stores all go to shared memory / tensor memory.
 template <class C, class GEO, int MODE, bool TM, int BUF, class RecFn>
 __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
-                                          const std::uint32_t* pfA, const std::uint32_t* pfB, RecFn&& rec) {
+                                          const std::uint32_t* pfA, const std::uint32_t* pfB, int pf_room,
+                                          RecFn&& rec) {
   constexpr int LB = GEO::LB, R = GEO::R;
   constexpr std::uint32_t BIAS = 0x80008000u;
   constexpr std::uint32_t OFF2 = 0x02000200u;
@@ -276,10 +279,23 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   }
   // The words of this buffer are consumed: refill it with block blk + 2 now,
   // so two full blocks of work cover the HBM latency.
+  // pf_room = words left in the frame window from pf: near the window end the
+  // prefetch is clamped so it never reads past the LLRs the caller provided.
+  if (pf_room >= LB / 2) {
 #pragma unroll
-  for (int i = 0; i < LB / 2; ++i) {
-    st.llr[BUF][0][i] = ldg_pinned(pfA + i);
-    st.llr[BUF][1][i] = ldg_pinned(pfB + i);
+    for (int i = 0; i < LB / 2; ++i) {
+      st.llr[BUF][0][i] = ldg_pinned(pfA + i);
+      st.llr[BUF][1][i] = ldg_pinned(pfB + i);
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < LB / 2; ++i) {
+      // re-read the window's last word (pf_room - 1 may be negative: still inside the
+      // frame); the values are never consumed past stage L-1.
+      const int o = i < pf_room ? i : pf_room - 1;
+      st.llr[BUF][0][i] = ldg_pinned(pfA + o);
+      st.llr[BUF][1][i] = ldg_pinned(pfB + o);
+    }
   }
 #pragma unroll
   for (int k = 0; k < LB; ++k) {
@@ -340,8 +356,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   std::uint32_t tbase = 0;
   if constexpr (TM) {
     if (warp == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
-          static_cast<unsigned>(__cvta_generic_to_shared(tmem_slot))));
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       static_cast<unsigned>(__cvta_generic_to_shared(tmem_slot))),
+                   "r"(static_cast<unsigned>(fp.tm_alloc)));
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -404,6 +421,10 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   // Prefetch pointers: block b + 2 is requested right after block b has
   // built its tables (two blocks of latency cover).
   const std::uint32_t* pfA = llrA + 2 * WPB;
+  // words of the frame window [0, L) stages: the word holding stage L-1 is the
+  // last one read (plan() keeps 2 stages of slack after every fast frame).
+  const int pf_last = (L - 1) / 2 + 1;  // one past the last word
+  int pf_off = 2 * WPB;
   const std::uint32_t* pfB = llrB + 2 * WPB;
 
   int next_sub = 0;
@@ -512,12 +533,13 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     // [v1, L) and on one side of the TMEM/smem split, no start stage inside.
     const bool clean = (t0 - 1 >= v1) && (t0 + LB - 2 < L) && !(next_rec >= t0 && next_rec < t0 + LB);
     if (clean && t0 - 1 >= t_split) {
-      run_block<C, GEO, 1, TM, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
+      run_block<C, GEO, 1, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     } else if (TM && clean && t0 + LB - 2 < t_split) {
-      run_block<C, GEO, 2, TM, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
+      run_block<C, GEO, 2, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     } else {
-      run_block<C, GEO, 0, TM, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
+      run_block<C, GEO, 0, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     }
+    pf_off += WPB;
     pfA += WPB;
     pfB += WPB;
     block_end(blk);
@@ -655,7 +677,10 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   if constexpr (TM) {
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tbase));
+    if (warp == 0) {
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tbase),
+                   "r"(static_cast<unsigned>(fp.tm_alloc)));
+    }
   }
 }
 
@@ -678,9 +703,39 @@ static_assert(K7a::sym() && K7b::sym() && K9a::sym() && K9b::sym() && K5a::sym()
               "fast-path codes must tap the newest and oldest register bits");
 
 constexpr int kMaxWarpsSmem = 8;   // smem-only survivor store
-constexpr int kWarpsTmem = 12;     // TMEM + smem survivor store: 3 warps per TMEM lane quarter
 constexpr int kSmemMax = 232448;   // sm_100 max dynamic shared memory per CTA
 constexpr int kHeader = 16;        // CTA header: TMEM base address
+
+// Per-(host thread, device) side stream + fork/join events for the edge-frame
+// launches (re-entrant: every host thread has its own).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+
+inline SideStream* side_stream() {
+  struct Cache {
+    std::map<int, SideStream> m;
+    ~Cache() {
+      for (auto& kv : m) {
+        if (cudaSetDevice(kv.first) != cudaSuccess) continue;
+        cudaEventDestroy(kv.second.fork);
+        cudaEventDestroy(kv.second.join);
+        cudaStreamDestroy(kv.second.s);
+      }
+    }
+  };
+  thread_local Cache cache;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  auto it = cache.m.find(dev);
+  if (it != cache.m.end()) return &it->second;
+  SideStream ss;
+  if (cudaStreamCreateWithFlags(&ss.s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+  if (cudaEventCreateWithFlags(&ss.fork, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  if (cudaEventCreateWithFlags(&ss.join, cudaEventDisableTiming) != cudaSuccess) return nullptr;
+  return &(cache.m[dev] = ss);
+}
 
 struct Plan {
   FastParams fp;
@@ -698,10 +753,11 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   fp.step = p.f0 > 0 ? p.f0 : p.f;
   fp.num_sub = (p.f + fp.step - 1) / fp.step;
   if (fp.num_sub > 64) return false;
+  if (fp.L < 2 * GEO::LB) return false;  // the first two blocks are loaded unclamped
   // Interior frames: full window, 4-byte aligned LLRs, prefetch in bounds.
   if ((static_cast<std::int64_t>(p.f) * 2) % 4 != 0 || (static_cast<std::int64_t>(p.v1) * 2) % 4 != 0) return false;
   if ((p.llr_stage0 * 2) % 4 != 0) return false;
-  const std::int64_t span = static_cast<std::int64_t>(fp.nblk + 2) * GEO::LB;  // stages read per frame
+  const std::int64_t span = static_cast<std::int64_t>(fp.L) + 2;  // stages read per frame (word granularity slack)
   std::int64_t lo = (p.v1 + p.f - 1) / p.f;                                    // first m with m*f >= v1
   std::int64_t hi_excl = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // m*f + f + v2 <= n
   // the caller guarantees LLRs up to the window end of the last launched frame
@@ -723,19 +779,35 @@ bool plan(const DecodeLaunch& p, Plan* out) {
     fp.ss_off = dec_bytes + x_bytes;
     fp.smem_per_warp = (dec_bytes + x_bytes + ss_bytes + 15) & ~15;
   };
-  // Preferred: 12 warps per CTA (3 per SMSP), survivors split between tensor
-  // memory (168 columns per warp) and shared memory.
-  fp.tcols = ((512 / (kWarpsTmem / 4)) & ~3);
-  fp.t_first = p.v1 & ~3;
-  fp.t_split = fp.t_first + fp.tcols;
-  fp.s_base = fp.t_split;
-  layout(std::max(fp.L - fp.t_split, 0) + 1);
-  if (kHeader + static_cast<std::size_t>(fp.smem_per_warp) * kWarpsTmem <= static_cast<std::size_t>(kSmemMax)) {
-    fp.warps_per_cta = kWarpsTmem;
-    out->tm = true;
-  } else {
+  // Tensor-memory survivor store: W warps per CTA (W/4 per TMEM lane quarter)
+  // share `alloc` columns. Large launches take 12 warps / 512 columns (one CTA
+  // and 12 warps per SM); small launches spread over more SMs.
+  const std::int64_t warps_needed = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
+  struct Cand {
+    int w, alloc;
+  };
+  const Cand cands[] = {{12, 512}, {8, 512}, {4, 256}};
+  bool ok = false;
+  for (const Cand& c : cands) {
+    const bool last = &c == &cands[2];
+    if (!last && warps_needed < static_cast<std::int64_t>(c.w) * 148) continue;  // would not fill the GPU
+    fp.tm_alloc = c.alloc;
+    fp.tcols = ((c.alloc / (c.w / 4)) & ~3);
+    fp.t_first = p.v1 & ~3;
+    fp.t_split = fp.t_first + fp.tcols;
+    fp.s_base = fp.t_split;
+    layout(std::max(fp.L - fp.t_split, 0) + 1);
+    if (kHeader + static_cast<std::size_t>(fp.smem_per_warp) * c.w <= static_cast<std::size_t>(kSmemMax)) {
+      fp.warps_per_cta = c.w;
+      out->tm = true;
+      ok = true;
+      break;
+    }
+  }
+  if (!ok) {
     // Long frames: shared memory only, as many warps as fit.
     fp.tcols = 0;
+    fp.tm_alloc = 0;
     fp.t_first = fp.t_split = fp.s_base = p.v1;
     layout(p.f + p.v2 + 1);
     const int w = (kSmemMax - kHeader) / fp.smem_per_warp;
@@ -754,17 +826,29 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   Plan pl;
   if (!plan<C, R>(p, &pl)) return cudaErrorNotSupported;
   const FastParams& fp = pl.fp;
-  // Edge frames (clipped windows) go to the generic kernel, on the same stream.
+  // Edge frames (clipped windows) go to the generic kernel on a side stream,
+  // concurrently with the fast kernel (they fit beside its CTA on an SM).
+  const bool edges = fp.mi0 > p.frame_begin || fp.mi1 < p.frame_end;
+  SideStream* side = nullptr;
+  if (edges) {
+    side = side_stream();
+    if (!side) return cudaErrorUnknown;
+    if (cudaError_t err = cudaEventRecord(side->fork, stream); err != cudaSuccess) return err;
+    if (cudaError_t err = cudaStreamWaitEvent(side->s, side->fork, 0); err != cudaSuccess) return err;
+  }
   if (fp.mi0 > p.frame_begin) {
     DecodeLaunch e = p;
     e.frame_end = fp.mi0;
-    if (cudaError_t err = launch_generic_i8(e, stream); err != cudaSuccess) return err;
+    if (cudaError_t err = launch_generic_i8(e, side->s); err != cudaSuccess) return err;
   }
   if (fp.mi1 < p.frame_end) {
     DecodeLaunch e = p;
     e.frame_begin = fp.mi1;
     if (p.sigma) e.sigma = static_cast<std::int64_t*>(p.sigma) + (fp.mi1 - p.frame_begin) * p.s;
-    if (cudaError_t err = launch_generic_i8(e, stream); err != cudaSuccess) return err;
+    if (cudaError_t err = launch_generic_i8(e, side->s); err != cudaSuccess) return err;
+  }
+  if (edges) {
+    if (cudaError_t err = cudaEventRecord(side->join, side->s); err != cudaSuccess) return err;
   }
   const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
   const std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
@@ -772,7 +856,9 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem));
   if (e != cudaSuccess) return e;
   kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fp);
-  return cudaGetLastError();
+  e = cudaGetLastError();
+  if (e == cudaSuccess && edges) e = cudaStreamWaitEvent(stream, side->join, 0);
+  return e;
 }
 
 template <class C, int R>

@@ -31,7 +31,8 @@
 namespace vd {
 namespace {
 
-constexpr int kWarps = 4;  // warps (frames in flight) per CTA
+constexpr int kWarps = 4;     // warps (frames in flight) per CTA
+constexpr int kStage = 128;   // LLR staging depth (stages) per warp
 constexpr unsigned kFull = 0xffffffffu;
 
 struct GenericParams {
@@ -42,6 +43,7 @@ struct GenericParams {
   bool dec_in_smem;
   std::uint32_t* dec_global;  // [total_warps][len_max * words] when !dec_in_smem
   int smem_per_warp;          // bytes
+  int stage_off, dec_off;     // byte offsets inside a warp's area
 };
 
 template <typename M>
@@ -67,7 +69,10 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
   M* sig1 = sig0 + S;
   M* table = sig1 + S;
   int* start_state = reinterpret_cast<int*>(table + nt);
-  std::uint32_t* dec = reinterpret_cast<std::uint32_t*>(start_state + gp.nsub_max + (gp.nsub_max & 1));
+  // LLR staging: kStage stages of this frame's window, loaded cooperatively
+  // (coalesced) by the warp once per kStage stages.
+  In* stage_buf = reinterpret_cast<In*>(base + gp.stage_off);
+  std::uint32_t* dec = reinterpret_cast<std::uint32_t*>(base + gp.dec_off);
   const std::int64_t gwarp = static_cast<std::int64_t>(blockIdx.x) * kWarps + warp;
   if (!gp.dec_in_smem) dec = gp.dec_global + gwarp * static_cast<std::int64_t>(gp.len_max) * words;
 
@@ -86,7 +91,14 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
     __syncwarp();
 
     for (std::int64_t t = 0; t < len; ++t) {
-      const In* lt = llr + (g.beg + t - p.llr_stage0) * p.b;
+      if ((t & (kStage - 1)) == 0) {
+        const std::int64_t cnt = imin(kStage, len - t) * p.b;
+        const In* src = llr + (g.beg + t - p.llr_stage0) * p.b;
+        __syncwarp();
+        for (std::int64_t i = lane; i < cnt; i += 32) stage_buf[i] = src[i];
+        __syncwarp();
+      }
+      const In* lt = stage_buf + (t & (kStage - 1)) * p.b;
       // Stage table (decoder.cpp:41-51): direct half, then complements.
       for (std::uint32_t bo = lane; bo < half; bo += 32) {
         M acc = M(0);
@@ -219,10 +231,14 @@ cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
 
   const std::size_t head = sizeof(M) * (2 * p.s + (1 << p.b)) + sizeof(int) * (gp.nsub_max + (gp.nsub_max & 1));
   const std::size_t head_al = (head + 15) & ~std::size_t(15);
+  const std::size_t stage_bytes = (sizeof(In) * kStage * p.b + 15) & ~std::size_t(15);
+  gp.stage_off = static_cast<int>(head_al);
+  gp.dec_off = static_cast<int>(head_al + stage_bytes);
   const std::size_t dec_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>(len_max) * gp.words;
   constexpr std::size_t kSmemBudget = 200 * 1024;
-  gp.dec_in_smem = (head_al + dec_bytes) * kWarps <= kSmemBudget;
-  const std::size_t per_warp = ((gp.dec_in_smem ? head_al + dec_bytes : head_al) + 15) & ~std::size_t(15);
+  gp.dec_in_smem = (head_al + stage_bytes + dec_bytes) * kWarps <= kSmemBudget;
+  const std::size_t per_warp =
+      ((gp.dec_in_smem ? head_al + stage_bytes + dec_bytes : head_al + stage_bytes) + 15) & ~std::size_t(15);
   if (per_warp * kWarps > kSmemBudget) return cudaErrorInvalidValue;  // K too large for this kernel
   gp.smem_per_warp = static_cast<int>(per_warp);
 
