@@ -40,6 +40,15 @@ F, V1, V2 = 256, 20, 20
 SCALE = 32.0
 EBN0 = 3.0
 
+# BASELINE.json configs that fit one GPU. C5 (the default) is the headline;
+# the others are measured with --workload for DESIGN.md (same metric).
+WORKLOADS = {
+    "C5": ((7, 2, [0o171, 0o133]), 1 << 32, "C5: K=7 r1/2 (171,133) framed decode, f=256 v1=20 v2=20 serial traceback"),
+    "C1": ((7, 2, [0o171, 0o133]), 1_000_000, "C1: K=7 r1/2 (171,133), 1M info bits, f=256 v1=20 v2=20"),
+    "C3": ((7, 3, [0o133, 0o171, 0o165]), 1 << 26, "C3: K=7 r1/3 (133,171,165), 64 Mi info bits, f=256 v1=20 v2=20"),
+    "C4": ((9, 2, [0o561, 0o753]), 1 << 28, "C4: K=9 r1/2 (561,753), 256 Mi info bits, f=256 v1=20 v2=20"),
+}
+
 
 def parse():
     ap = argparse.ArgumentParser()
@@ -47,12 +56,17 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--stages", type=int, default=1 << 32, help="info bits per rank per step")
+    ap.add_argument("--workload", choices=sorted(WORKLOADS), default="C5")
+    ap.add_argument("--stages", type=int, default=0, help="info bits per rank per step (0: the workload's)")
     ap.add_argument("--e2e-stages", type=int, default=1 << 30, help="info bits per e2e step (host buffers)")
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
-    return ap.parse_args()
+    a = ap.parse_args()
+    a.code, default_n, a.workload_desc = WORKLOADS[a.workload]
+    if a.stages <= 0:
+        a.stages = default_n
+    return a
 
 
 def measured_peaks():
@@ -121,7 +135,7 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU arms -----
 
-def cpu_reference_rate(target_s: float, threads: int | None = None):
+def cpu_reference_rate(target_s: float, threads: int | None = None, code=K7):
     """The reference framed_decode (oracle/_ref, all host threads) or, if the
     reference library is absent, the single-threaded C oracle port. Returns
     (Gbps, cores, kind, sample description)."""
@@ -138,18 +152,18 @@ def cpu_reference_rate(target_s: float, threads: int | None = None):
     backend = ref if ref is not None else port
     # probe on a small block, then size the sample for ~target_s of wall time
     n = 1 << 16
-    rx, _ = port.gen_bench_block(*K7, n, EBN0, 1)
+    rx, _ = port.gen_bench_block(*code, n, EBN0, 1)
     q = oracle.quantize(rx, SCALE)
     t0 = time.perf_counter()
-    backend.framed_decode(*K7, q, n, F, V1, V2, workers=cores)
+    backend.framed_decode(*code, q, n, F, V1, V2, workers=cores)
     rate = n / max(time.perf_counter() - t0, 1e-6)
     n = int(min(max(rate * target_s, 1 << 16), 1 << 26))
-    rx, _ = port.gen_bench_block(*K7, n, EBN0, 2)
+    rx, _ = port.gen_bench_block(*code, n, EBN0, 2)
     q = oracle.quantize(rx, SCALE)
     t0 = time.perf_counter()
-    backend.framed_decode(*K7, q, n, F, V1, V2, workers=cores)
+    backend.framed_decode(*code, q, n, F, V1, V2, workers=cores)
     dt = time.perf_counter() - t0
-    sample = (f"{n} info bits (K=7 r1/2, int8 q=rint(32y) at {EBN0} dB, f={F}/v1={V1}/v2={V2}), "
+    sample = (f"{n} info bits (K={code[0]} B={code[1]}, int8 q=rint(32y) at {EBN0} dB, f={F}/v1={V1}/v2={V2}), "
               f"{'reference framed_decode, workers=' + str(cores) if ref else 'C oracle port, 1 thread'}")
     return n / dt / 1e9, cores, kind, sample, dt
 
@@ -205,17 +219,18 @@ def run_ours(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
 
-    t = vd.build_trellis(vd.CodeSpec(*K7))
+    t = vd.build_trellis(vd.CodeSpec(*args.code))
+    B = args.code[1]
     cfg = vd.FrameConfig(F, V1, V2)
     n = args.stages
     nf = (n + F - 1) // F
     stats = vd.frame_stats(cfg, n)
     stream = torch.cuda.Stream(device=dev)
-    llr = torch.empty(n * 2, dtype=torch.int8, device=dev)
+    llr = torch.empty(n * B, dtype=torch.int8, device=dev)
     bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
     out = torch.empty((n + 31) // 32 + 1, dtype=torch.int32, device=dev)
     with torch.cuda.stream(stream):
-        synth_llr_i8(t, n, (1.0 / (2 * 0.5 * 10 ** (EBN0 / 10))) ** 0.5, SCALE, 1234 + rank, llr, bits, local, stream)
+        synth_llr_i8(t, n, (1.0 / (2 * (1.0 / B) * 10 ** (EBN0 / 10))) ** 0.5, SCALE, 1234 + rank, llr, bits, local, stream)
     stream.synchronize()
 
     def step():
@@ -254,8 +269,8 @@ def run_ours(args):
 
     # ---- e2e through the host-buffer C-ABI call (pinned memory) -----------
     ne = min(args.e2e_stages, n)
-    host_llr = torch.empty(ne * 2, dtype=torch.int8, pin_memory=True)
-    host_llr.copy_(llr[: ne * 2])
+    host_llr = torch.empty(ne * B, dtype=torch.int8, pin_memory=True)
+    host_llr.copy_(llr[: ne * B])
     host_out = torch.empty((ne + 31) // 32, dtype=torch.int32, pin_memory=True)
     lib = vd.lib()
     c = cfg.to_c()
@@ -296,24 +311,25 @@ def run_ours(args):
     alu_peak = sms * 384 * sm_mhz * 1e6 / 1e12
     alu_src = (f"{sms} SM x 384 packed-ACS lane-ops/clk (ncu-measured pipe rates, profiles/r01_pipe_probe_ncu.csv) "
                f"x {sm_mhz:.0f} MHz (median SM clock during the timed region)")
-    ops_bit = alu_ops_per_bit(stats.stages, n)
+    ops_bit = alu_ops_per_bit(stats.stages, n, 1 << (args.code[0] - 1))
     bits_per_s_kernel = n / (ms_step * 1e-3)
     alu_achieved = ops_bit * bits_per_s_kernel / 1e12
-    hbm_bytes = n * 2 + n / 8  # int8 LLR read once + packed output
+    hbm_bytes = n * B + n / 8  # int8 LLR read once + packed output
     hbm_achieved = hbm_bytes / (ms_step * 1e-3) / 1e9
     traffic = None
     tp = ROOT / "profiles" / "decode_traffic.json"
-    if tp.exists():
+    if tp.exists() and args.workload == "C5":
         traffic = json.loads(tp.read_text()).get("bytes_per_bit", 0) * n
 
     result = None
     if rank == 0:
         cpu = None
         if not args.no_cpu:
-            g, cores, kind, sample, _ = cpu_reference_rate(args.cpu_seconds)
+            g, cores, kind, sample, _ = cpu_reference_rate(args.cpu_seconds, code=args.code)
             cpu = {"value": g, "unit": "Gbps", "cores": cores, "kind": kind, "sample": sample}
         result = {
-            "metric": "decoded info Gbps (K=7 r1/2 soft)",
+            "metric": "decoded info Gbps (K=7 r1/2 soft)" if args.workload in ("C5", "C1") else
+                      f"decoded info Gbps (K={args.code[0]} B={args.code[1]} soft)",
             "value": gbps,
             "unit": "Gbps",
             "n_gpus": world,
@@ -326,11 +342,13 @@ def run_ours(args):
             "dtype": "int8 LLR / int32 path metrics" if not t.fast_path() else "int8 LLR / int16x2 path metrics",
             "data": "synthetic: random message, K=7 encoder, BPSK+AWGN at 3 dB, int8 q=rint(32y), generated in HBM",
             "config": {
-                "workload": "C5: K=7 r1/2 (171,133) framed decode, f=256 v1=20 v2=20 serial traceback",
+                "workload": args.workload_desc,
                 "info_bits_per_gpu_per_step": n,
                 "frames_per_gpu": nf,
                 "parallelism": f"frame shards x{world} (no collective)",
-                "l2": "inputs (2 B/bit x 4 Gi = 8 GiB) exceed L2; no flush needed",
+                "l2": (f"inputs ({B} B/bit x {n} bits = {n * B / 2**30:.2f} GiB) exceed L2; no flush needed"
+                       if n * B > 256 << 20 else
+                       f"inputs ({n * B / 2**20:.1f} MiB) fit in L2: steps re-read them warm (latency-bound size)"),
                 "kernel": "fast (register-resident)" if t.fast_path() else "generic (warp per frame)",
                 "ber_check": ber,
             },
@@ -348,7 +366,7 @@ def run_ours(args):
                         "peak_source": peak_src},
             },
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_gbps, "unit": "Gbps", "h2d_bytes_per_step": ne * 2,
+            "e2e": {"value": e2e_gbps, "unit": "Gbps", "h2d_bytes_per_step": ne * B,
                     "d2h_bytes_per_step": ((ne + 31) // 32) * 4, "info_bits_per_step": ne,
                     "matches_device_decode": same},
             "gpu_launches": 3 * args.steps,  # per step: head/tail edge frames (generic) + fast kernel

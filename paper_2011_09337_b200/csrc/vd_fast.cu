@@ -51,19 +51,33 @@ __device__ __forceinline__ std::uint32_t prmt(std::uint32_t a, std::uint32_t b, 
 
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
-/// Rate-1/2 code with compile-time generator polynomials.
-template <int K_, std::uint32_t P0, std::uint32_t P1>
-struct Code2 {
+/// Rate-1/B code (B = 2 or 3) with compile-time generator polynomials.
+template <int K_, int B_, std::uint32_t P0, std::uint32_t P1, std::uint32_t P2 = 0>
+struct CodeB {
   static constexpr int kK = K_;
-  static constexpr int kB = 2;
+  static constexpr int kB = B_;
+  static constexpr std::uint32_t kXM = (1u << B_) - 1u;  // complement mask of a branch index
+  static constexpr std::uint32_t poly(int i) { return i == 0 ? P0 : i == 1 ? P1 : P2; }
   // Branch-index bits contributed by register bit q (poly 0 -> MSB of the
   // index, as reference trellis.cpp:70-73 packs branch outputs).
-  static constexpr std::uint32_t cb(int q) { return (((P0 >> q) & 1u) << 1) | ((P1 >> q) & 1u); }
-  static constexpr bool sym() { return cb(0) == 3u && cb(K_ - 1) == 3u; }
+  static constexpr std::uint32_t cb(int q) {
+    std::uint32_t x = 0;
+    for (int i = 0; i < B_; ++i) x |= ((poly(i) >> q) & 1u) << (B_ - 1 - i);
+    return x;
+  }
+  static constexpr bool sym() { return cb(0) == kXM && cb(K_ - 1) == kXM; }
   static constexpr bool matches(int k, int b, const std::uint32_t* p) {
-    return k == K_ && b == 2 && p[0] == P0 && p[1] == P1;
+    if (k != K_ || b != B_) return false;
+    for (int i = 0; i < B_; ++i) {
+      if (p[i] != poly(i)) return false;
+    }
+    return true;
   }
 };
+template <int K_, std::uint32_t P0, std::uint32_t P1>
+using Code2 = CodeB<K_, 2, P0, P1>;
+template <int K_, std::uint32_t P0, std::uint32_t P1, std::uint32_t P2>
+using Code3 = CodeB<K_, 3, P0, P1, P2>;
 
 template <class C, int R_>
 struct Geo {
@@ -74,6 +88,9 @@ struct Geo {
   static constexpr int g = M - r;
   static constexpr int G = 1 << g;
   static constexpr int LB = r;            // stages per block
+  static constexpr int B = C::kB;
+  static constexpr int WPB = LB * B / 4;  // LLR words per frame per block (4 stages x B bytes)
+  static constexpr int NT = 1 << (B - 1); // direct branch-table entries per stage
   static constexpr int GROUPS = 32 / G;   // lane groups (frame pairs) per warp
   static constexpr int FPW = 2 * GROUPS;  // frames per warp
   static constexpr std::uint32_t SMASK = S - 1;
@@ -197,6 +214,12 @@ __device__ __forceinline__ std::uint32_t bitsel(std::uint32_t a, std::uint32_t b
 }
 
 // 32 decisions (16 registers x 2 frames) -> one word, bit (rho + 16 * half).
+// The source words carry !decision in bits 15 / 31; the last merge inverts.
+__device__ __forceinline__ std::uint32_t bitsel_not(std::uint32_t a, std::uint32_t b) {
+  std::uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0x1B;" : "=r"(r) : "r"(a), "r"(b), "n"(0x0f0f0f0fu));  // ~(c ? a : b)
+  return r;
+}
 __device__ __forceinline__ std::uint32_t compact16(const std::uint32_t* w) {
   std::uint32_t y[8];
 #pragma unroll
@@ -207,16 +230,62 @@ __device__ __forceinline__ std::uint32_t compact16(const std::uint32_t* w) {
   const std::uint32_t d = bitsel<0x40404040u>(y[6], y[7]);
   const std::uint32_t ab = bitsel<0x03030303u>(a, b);
   const std::uint32_t cd = bitsel<0x30303030u>(c, d);
-  return bitsel<0x0f0f0f0fu>(ab, cd);
+  return bitsel_not(ab, cd);
 }
 
 template <class GEO>
 struct FrameState {
   std::uint32_t sig[GEO::R];
   std::uint32_t wv[2][GEO::R];
-  std::uint32_t fm[GEO::LB], k0[GEO::LB], k1[GEO::LB];  // per-lane LLR flip constants per phase
-  std::uint32_t llr[2][2][GEO::LB / 2];                  // [buffer][frame A/B][word]: even/odd blocks
+  // Per-lane LLR sign flips (lane part of the branch index): fw[j] XORs the
+  // block's raw LLR word j (0x80: int8 -> offset binary; 0xff: one's-complement
+  // negation), kc[k][e] are the per-phase corrections that make the one's
+  // complement exact inside the table sums.
+  std::uint32_t fw[GEO::WPB];
+  std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : 3];
+  std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
 };
+
+// Branch tables of one block: PT[k][x] = T_k[x ^ lane part] + 128 B per half
+// (T = the reference stage table, decoder.cpp:41-51, for frames A | B).
+template <class C, class GEO, int BUF>
+__device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uint32_t (&PT)[GEO::LB][1 << GEO::B]) {
+  constexpr int LB = GEO::LB, B = GEO::B, WPB = GEO::WPB;
+  constexpr std::uint32_t XM = C::kXM;
+  constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * B) * 0x00010001u;
+  // interleave frames A / B: lo = (A0, A1, B0, B1), hi = (A2, A3, B2, B3) of each word
+  std::uint32_t il[WPB][2];
+#pragma unroll
+  for (int j = 0; j < WPB; ++j) {
+    const std::uint32_t a = st.llr[BUF][0][j] ^ st.fw[j];
+    const std::uint32_t b = st.llr[BUF][1][j] ^ st.fw[j];
+    il[j][0] = prmt(a, b, 0x5410u);
+    il[j][1] = prmt(a, b, 0x7632u);
+  }
+  // LLR i of phase k, zero-extended per half: byte q = k B + i of the block
+  auto X = [&](int k, int i) {
+    const int q = k * B + i;
+    return prmt(il[q >> 2][(q >> 1) & 1], 0u, (q & 1) ? 0x4341u : 0x4240u);
+  };
+#pragma unroll
+  for (int k = 0; k < LB; ++k) {
+    const std::uint32_t x0 = X(k, 0), x1 = X(k, 1);
+    if constexpr (B == 2) {
+      PT[k][0] = x0 + x1 + st.kc[k][0];             // l0 + l1 + 256
+      PT[k][1] = x0 - x1 + st.kc[k][1];             // l0 - l1 + 256
+    } else {
+      const std::uint32_t x2 = X(k, 2) + st.kc[k][2];
+      const std::uint32_t a = x0 + x1 + st.kc[k][0];  // l0 + l1 + 256
+      const std::uint32_t d = x0 - x1 + st.kc[k][1];  // l0 - l1 + 256
+      PT[k][0] = a + x2;
+      PT[k][1] = a - x2 + 0x01000100u;
+      PT[k][2] = d + x2;
+      PT[k][3] = d - x2 + 0x01000100u;
+    }
+#pragma unroll
+    for (int x = 0; x < GEO::NT; ++x) PT[k][x ^ XM] = OFFB - PT[k][x];  // T[x ^ XM] = -T[x]
+  }
+}
 
 // ---- tensor-memory survivor store --------------------------------------------
 __device__ __forceinline__ void tmem_st1(std::uint32_t taddr, std::uint32_t v) {
@@ -257,39 +326,24 @@ template <class C, class GEO, int MODE, bool TM, int BUF, class RecFn>
 __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
                                           const std::uint32_t* pfA, const std::uint32_t* pfB, int pf_room,
                                           RecFn&& rec) {
-  constexpr int LB = GEO::LB, R = GEO::R;
-  constexpr std::uint32_t BIAS = 0x80008000u;
-  constexpr std::uint32_t OFF2 = 0x02000200u;
+  constexpr int LB = GEO::LB, R = GEO::R, WPB = GEO::WPB;
+  constexpr std::uint32_t XM = C::kXM;
   // ---- branch-metric tables for the LB stages of this block (both frames) ---
-  std::uint32_t PT[LB][4], CL[LB][4];
-#pragma unroll
-  for (int k = 0; k < LB; ++k) {
-    const std::uint32_t wA = st.llr[BUF][0][k >> 1], wB = st.llr[BUF][1][k >> 1];
-    const std::uint32_t o = (k & 1) * 2;
-    const std::uint32_t sel = o | ((o + 1) << 4) | ((o + 4) << 8) | ((o + 5) << 12);
-    const std::uint32_t tmp = prmt(wA, wB, sel) ^ st.fm[k];
-    const std::uint32_t X = prmt(tmp, 0u, 0x4240u);  // (L0A, L0B) offset-binary, zero-extended
-    const std::uint32_t Y = prmt(tmp, 0u, 0x4341u);  // (L1A, L1B)
-    PT[k][0] = X + Y + st.k0[k];                     // T0 + 256 = l0 + l1 + 256
-    PT[k][1] = X + (Y ^ 0x00ff00ffu) + st.k1[k];     // T1 + 256 = l0 - l1 + 256
-    PT[k][3] = OFF2 - PT[k][0];                      // T3 = -T0
-    PT[k][2] = OFF2 - PT[k][1];                      // T2 = -T1
-#pragma unroll
-    for (int x = 0; x < 4; ++x) CL[k][x] = PT[k][x ^ 3] - PT[k][x] + BIAS;
-  }
+  std::uint32_t PT[LB][1 << GEO::B];
+  block_tables<C, GEO, BUF>(st, PT);
   // The words of this buffer are consumed: refill it with block blk + 2 now,
   // so two full blocks of work cover the HBM latency.
   // pf_room = words left in the frame window from pf: near the window end the
   // prefetch is clamped so it never reads past the LLRs the caller provided.
-  if (pf_room >= LB / 2) {
+  if (pf_room >= WPB) {
 #pragma unroll
-    for (int i = 0; i < LB / 2; ++i) {
+    for (int i = 0; i < WPB; ++i) {
       st.llr[BUF][0][i] = ldg_pinned(pfA + i);
       st.llr[BUF][1][i] = ldg_pinned(pfB + i);
     }
   } else {
 #pragma unroll
-    for (int i = 0; i < LB / 2; ++i) {
+    for (int i = 0; i < WPB; ++i) {
       // re-read the window's last word (pf_room - 1 may be negative: still inside the
       // frame); the values are never consumed past stage L-1.
       const int o = i < pf_room ? i : pf_room - 1;
@@ -308,12 +362,17 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       const int od = e | (1 << k);
       const std::uint32_t x = GEO::xreg(k, e);
       const std::uint32_t sE = st.sig[e], sO = st.sig[od];
-      const std::uint32_t s2L = __vadd2(sO, PT[k][x ^ 3]);
+      const std::uint32_t s2L = __vadd2(sO, PT[k][x ^ XM]);
       const std::uint32_t s2H = __vadd2(sO, PT[k][x]);
-      w[e] = sO - sE + CL[k][x];
-      w[od] = sO - sE + CL[k][x ^ 3];
-      st.sig[e] = __viaddmax_s16x2(sE, PT[k][x], s2L);
-      st.sig[od] = __viaddmax_s16x2(sE, PT[k][x ^ 3], s2H);
+      const std::uint32_t nL = __viaddmax_s16x2(sE, PT[k][x], s2L);
+      const std::uint32_t nH = __viaddmax_s16x2(sE, PT[k][x ^ XM], s2H);
+      // new - second candidate >= 0 per half, 0 iff the second predecessor
+      // won (ties included, decoder.cpp:67-74); + 0x7FFF per half moves
+      // "nonzero" into bit 15 / 31 without a carry between the halves.
+      w[e] = nL - s2L + 0x7fff7fffu;
+      w[od] = nH - s2H + 0x7fff7fffu;
+      st.sig[e] = nL;
+      st.sig[od] = nH;
     }
     // ---- previous stage's decisions -> survivor store (overlaps this ACS) --
     const std::uint32_t word = compact16(st.wv[(k + 1) & 1]);
@@ -335,8 +394,8 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   using GEO = Geo<C, R>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, r = GEO::r, g = GEO::g;
   constexpr std::uint32_t BASE = 0x20002000u;  // offset-binary metric origin (8192 per half)
-  constexpr int WPB = LB / 2;
-  static_assert(LB % 2 == 0, "B=2 fast path needs an even block length");
+  constexpr int WPB = GEO::WPB, B = GEO::B;
+  static_assert((LB * B) % 4 == 0, "a block must cover whole LLR words");
   static_assert(LB == 4, "tensor-memory blocks are 4 columns");
   static_assert(R == 16, "one 32-bit decision word per lane per stage");
   const DecodeLaunch& p = fp.p;
@@ -386,23 +445,37 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   const int s_base = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.s_base)));
   // Frame-relative LLR word pointers (frame start is 4-byte aligned: checked at launch).
   const std::uint32_t* llrA = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
-                                                                     (lA * f - v1 - p.llr_stage0) * 2);
+                                                                     (lA * f - v1 - p.llr_stage0) * B);
   const std::uint32_t* llrB = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
-                                                                     (lB * f - v1 - p.llr_stage0) * 2);
+                                                                     (lB * f - v1 - p.llr_stage0) * B);
 
   FrameState<GEO> st;
   // Per-phase flip constants for this lane (lane part of the branch index).
+  {
+    std::uint32_t fw[WPB];
 #pragma unroll
-  for (int k = 0; k < LB; ++k) {
-    std::uint32_t z = 0;
+    for (int j = 0; j < WPB; ++j) fw[j] = 0x80808080u;
 #pragma unroll
-    for (int i = 0; i < g; ++i) {
-      if ((lam >> i) & 1) z ^= C::cb(r + i - k);
+    for (int k = 0; k < LB; ++k) {
+      std::uint32_t z = 0;  // lane part of the branch index at phase k
+#pragma unroll
+      for (int i = 0; i < g; ++i) {
+        if ((lam >> i) & 1) z ^= C::cb(r + i - k);
+      }
+      std::uint32_t phi[3] = {0u, 0u, 0u};  // llr i negated for this lane
+#pragma unroll
+      for (int i = 0; i < B; ++i) {
+        phi[i] = (z >> (B - 1 - i)) & 1u;
+        const int q = k * B + i;
+        if (phi[i]) fw[q >> 2] ^= 0xffu << (8 * (q & 3));
+      }
+      // one's complement (255 - u) is the exact negation (256 - u) minus 1
+      st.kc[k][0] = opaque((phi[0] + phi[1]) * 0x00010001u);
+      st.kc[k][1] = opaque((256u + phi[0] - phi[1]) * 0x00010001u);
+      if constexpr (B == 3) st.kc[k][2] = opaque(phi[2] * 0x00010001u);
     }
-    const std::uint32_t f0b = (z >> 1) & 1u, f1b = z & 1u;  // flip l0 / flip l1
-    st.fm[k] = opaque(0x80808080u ^ (f0b ? 0x00ff00ffu : 0u) ^ (f1b ? 0xff00ff00u : 0u));
-    st.k0[k] = opaque((f0b + f1b) * 0x00010001u);
-    st.k1[k] = opaque((f0b + 1u - f1b) * 0x00010001u);
+#pragma unroll
+    for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
   }
 #pragma unroll
   for (int i = 0; i < R; ++i) st.sig[i] = BASE;
@@ -423,7 +496,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   const std::uint32_t* pfA = llrA + 2 * WPB;
   // words of the frame window [0, L) stages: the word holding stage L-1 is the
   // last one read (plan() keeps 2 stages of slack after every fast frame).
-  const int pf_last = (L - 1) / 2 + 1;  // one past the last word
+  const int pf_last = (L * B - 1) / 4 + 1;  // one past the last word
   int pf_off = 2 * WPB;
   const std::uint32_t* pfB = llrB + 2 * WPB;
 
@@ -463,13 +536,13 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
       sstate[(2 * grp + 1) * num_sub + next_sub] = static_cast<std::uint16_t>(0xffffu - (bestB & 0xffffu));
     }
     if (t == L - 1 && p.sigma != nullptr) {
-      // final metrics: true = stored - BASE - 256 * L + sum(ref - BASE)
+      // final metrics: true = stored - BASE - 128 B L + sum(ref - BASE)
       std::int64_t* sg = static_cast<std::int64_t*>(p.sigma);
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         const int sidx = static_cast<int>(lanepart | static_cast<std::uint32_t>(GEO::rotr(i, k + 1)));
-        const std::int64_t a = static_cast<std::int64_t>(st.sig[i] & 0xffffu) - 8192 - 256LL * L + subA;
-        const std::int64_t b = static_cast<std::int64_t>(st.sig[i] >> 16) - 8192 - 256LL * L + subB;
+        const std::int64_t a = static_cast<std::int64_t>(st.sig[i] & 0xffffu) - 8192 - 128LL * B * L + subA;
+        const std::int64_t b = static_cast<std::int64_t>(st.sig[i] >> 16) - 8192 - 128LL * B * L + subB;
         if (validA) sg[(mA - p.frame_begin) * S + sidx] = a;
         if (validB) sg[(mB - p.frame_begin) * S + sidx] = b;
       }
@@ -699,7 +772,9 @@ using K9b = Code2<9, 0753, 0561>;
 using K5a = Code2<5, 023, 035>;
 using K6a = Code2<6, 053, 075>;
 using K8a = Code2<8, 0247, 0371>;
-static_assert(K7a::sym() && K7b::sym() && K9a::sym() && K9b::sym() && K5a::sym() && K6a::sym() && K8a::sym(),
+using K7c = Code3<7, 0133, 0171, 0165>;  // LTE rate 1/3
+static_assert(K7a::sym() && K7b::sym() && K9a::sym() && K9b::sym() && K5a::sym() && K6a::sym() && K8a::sym() &&
+                  K7c::sym(),
               "fast-path codes must tap the newest and oldest register bits");
 
 constexpr int kMaxWarpsSmem = 8;   // smem-only survivor store
@@ -755,9 +830,10 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   if (fp.num_sub > 64) return false;
   if (fp.L < 2 * GEO::LB) return false;  // the first two blocks are loaded unclamped
   // Interior frames: full window, 4-byte aligned LLRs, prefetch in bounds.
-  if ((static_cast<std::int64_t>(p.f) * 2) % 4 != 0 || (static_cast<std::int64_t>(p.v1) * 2) % 4 != 0) return false;
-  if ((p.llr_stage0 * 2) % 4 != 0) return false;
-  const std::int64_t span = static_cast<std::int64_t>(fp.L) + 2;  // stages read per frame (word granularity slack)
+  constexpr int B = GEO::B;
+  if ((static_cast<std::int64_t>(p.f) * B) % 4 != 0 || (static_cast<std::int64_t>(p.v1) * B) % 4 != 0) return false;
+  if ((p.llr_stage0 * B) % 4 != 0) return false;
+  const std::int64_t span = static_cast<std::int64_t>(fp.L) + 4;  // stages read per frame (word granularity slack)
   std::int64_t lo = (p.v1 + p.f - 1) / p.f;                                    // first m with m*f >= v1
   std::int64_t hi_excl = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // m*f + f + v2 <= n
   // the caller guarantees LLRs up to the window end of the last launched frame
@@ -874,8 +950,9 @@ bool try_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
 
 bool fast_path_supported(const DecodeLaunch& p) {
   using namespace fast;
-  if (p.b != 2) return false;
+  if (p.b != 2 && p.b != 3) return false;
   Plan pl;
+  if (K7c::matches(p.k, p.b, p.polys)) return plan<K7c, 16>(p, &pl);
   if (K7a::matches(p.k, p.b, p.polys)) return plan<K7a, 16>(p, &pl);
   if (K7b::matches(p.k, p.b, p.polys)) return plan<K7b, 16>(p, &pl);
   if (K9a::matches(p.k, p.b, p.polys)) return plan<K9a, 16>(p, &pl);
@@ -890,6 +967,7 @@ cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream) {
   using namespace fast;
   cudaError_t err = cudaErrorNotSupported;
   if (try_variant<K7a, 16>(p, stream, &err)) return err;
+  if (try_variant<K7c, 16>(p, stream, &err)) return err;
   if (try_variant<K7b, 16>(p, stream, &err)) return err;
   if (try_variant<K9a, 16>(p, stream, &err)) return err;
   if (try_variant<K9b, 16>(p, stream, &err)) return err;

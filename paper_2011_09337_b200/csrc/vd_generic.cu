@@ -214,6 +214,277 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
   }
 }
 
+// Register-resident variant for S <= 256 (K <= 9), the latency path for the
+// few edge frames around every fast-kernel launch and the throughput path for
+// the FP64 API. Same algorithm and outputs as generic_kernel above; lane j owns
+// states j, j+32, ... in registers, so the critical chain of a stage is
+// shuffle -> add -> compare -> select (no shared-memory round trip or
+// __syncwarp between stages). Branch metrics are evaluated per lane straight
+// from the stage LLRs in the reference's add order (decoder.cpp:41-51).
+template <typename In, typename M, int NPL>
+__global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp) {
+  const DecodeLaunch& p = gp.p;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+  const int S = p.s;
+  const int b = p.b;
+  const std::uint32_t half = 1u << (b - 1);
+  const std::uint32_t tmask = (1u << b) - 1u;
+
+  unsigned char* base = smem_raw + static_cast<std::size_t>(warp) * gp.smem_per_warp;
+  int* start_state = reinterpret_cast<int*>(base);
+  In* stage_buf = reinterpret_cast<In*>(base + gp.stage_off);
+  std::uint32_t* dec = reinterpret_cast<std::uint32_t*>(base + gp.dec_off);
+  const std::int64_t gwarp = static_cast<std::int64_t>(blockIdx.x) * kWarps + warp;
+  if (!gp.dec_in_smem) dec = gp.dec_global + gwarp * static_cast<std::int64_t>(gp.len_max) * NPL;
+
+  // Branch labels of this lane's states: table index (sign pattern) and
+  // whether the entry is the complement of the direct half.
+  std::uint32_t lab[NPL][2];
+  bool valid[NPL];
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) {
+    const int j = r * 32 + lane;
+    valid[r] = j < S;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const std::uint32_t x = valid[r] ? __ldg(p.in_out + 2 * j + e) : 0u;
+      lab[r][e] = x;
+    }
+  }
+  // predecessor lanes
+  const int low = S / 2 - 1;
+  const int srcA = NPL == 1 ? (((lane & low) << 1) & 31) : ((2 * lane) & 31);
+  const int srcB = NPL == 1 ? ((((lane & low) << 1) | 1) & 31) : ((2 * lane + 1) & 31);
+  const bool upper = lane >= 16;
+
+  const In* llr = static_cast<const In*>(p.llr);
+  const std::int64_t total_warps = static_cast<std::int64_t>(gridDim.x) * kWarps;
+
+  auto bm = [&](const M* v, std::uint32_t x) -> M {
+    const bool neg = x >= half;
+    const std::uint32_t xs = neg ? (x ^ tmask) : x;
+    M acc = M(0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i < b) acc += ((xs >> (b - 1 - i)) & 1u) ? -v[i] : v[i];
+    }
+    return neg ? -acc : acc;
+  };
+
+  for (std::int64_t m = p.frame_begin + gwarp; m < p.frame_end; m += total_warps) {
+    const FrameGeom g(m, p.n, p.f, p.v1, p.v2, p.f0);
+    const std::int64_t len = g.len();
+    M sig[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) sig[r] = M(0);  // sigma_0 = 0 (decoder.cpp:195)
+    std::int64_t offset = 0;
+    std::int64_t next_record = 0;
+    std::int64_t next_start = g.start_stage(0, p.v2);
+    const In* src = llr + (g.beg - p.llr_stage0) * b;
+
+    auto refill = [&](std::int64_t t) {
+      const std::int64_t cnt = imin(kStage, len - t) * b;
+      __syncwarp();
+      for (std::int64_t i = lane; i < cnt; i += 32) stage_buf[i] = src[t * b + i];
+      __syncwarp();
+    };
+    M v[8];
+    if (len > 0) {
+      refill(0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) v[i] = i < b ? static_cast<M>(stage_buf[i]) : M(0);
+    }
+    for (std::int64_t t = 0; t < len; ++t) {
+      M bmv[NPL][2];
+#pragma unroll
+      for (int r = 0; r < NPL; ++r) {
+        bmv[r][0] = bm(v, lab[r][0]);
+        bmv[r][1] = bm(v, lab[r][1]);
+      }
+      if (t + 1 < len) {  // software pipeline: next stage's LLRs
+        if (((t + 1) & (kStage - 1)) == 0) refill(t + 1);
+        const In* lt = stage_buf + ((t + 1) & (kStage - 1)) * b;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) v[i] = i < b ? static_cast<M>(lt[i]) : M(0);
+      }
+      // ACS (decoder.cpp:53-76): ties -> second predecessor.
+      M nsig[NPL];
+      bool d[NPL];
+#pragma unroll
+      for (int q = 0; q < (NPL == 1 ? 1 : NPL / 2); ++q) {
+        M pa, pb;
+        if constexpr (NPL == 1) {
+          pa = __shfl_sync(kFull, sig[0], srcA);
+          pb = __shfl_sync(kFull, sig[0], srcB);
+        } else {
+          const M a0 = __shfl_sync(kFull, sig[2 * q], srcA);
+          const M a1 = __shfl_sync(kFull, sig[2 * q + 1], srcA);
+          const M b0 = __shfl_sync(kFull, sig[2 * q], srcB);
+          const M b1 = __shfl_sync(kFull, sig[2 * q + 1], srcB);
+          pa = upper ? a1 : a0;
+          pb = upper ? b1 : b0;
+        }
+#pragma unroll
+        for (int h = 0; h < (NPL == 1 ? 1 : 2); ++h) {
+          const int r = q + h * (NPL / 2);
+          const M s1 = pa + bmv[r][0];
+          const M s2 = pb + bmv[r][1];
+          d[r] = !(s1 > s2);
+          nsig[r] = d[r] ? s2 : s1;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < NPL; ++r) {
+        sig[r] = nsig[r];
+        const std::uint32_t w = __ballot_sync(kFull, d[r] && valid[r]);
+        if (lane == r) dec[t * NPL + r] = w;
+      }
+      if constexpr (std::is_integral<M>::value) {
+        if ((t & 4095) == 4095) {  // int32 renormalisation (exact differences)
+          const M ref = __shfl_sync(kFull, sig[0], 0);
+#pragma unroll
+          for (int r = 0; r < NPL; ++r) sig[r] -= ref;
+          offset += ref;
+        }
+      }
+      // Stored-max start states (decoder.cpp:205-211): lowest index on ties.
+      while (next_record < g.num_sub && next_start == t) {
+        M bv = sig[0];
+        int bi = lane;
+        bool have = valid[0];
+#pragma unroll
+        for (int r = 1; r < NPL; ++r) {
+          if (valid[r] && (!have || sig[r] > bv)) {
+            bv = sig[r];
+            bi = r * 32 + lane;
+            have = true;
+          }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const M ov = __shfl_xor_sync(kFull, bv, o);
+          const int oi = __shfl_xor_sync(kFull, bi, o);
+          const bool oh = __shfl_xor_sync(kFull, have ? 1 : 0, o) != 0;
+          if (oh && (!have || better(ov, oi, bv, bi))) {
+            bv = ov;
+            bi = oi;
+            have = true;
+          }
+        }
+        if (lane == 0) start_state[next_record] = bi;
+        ++next_record;
+        if (next_record < g.num_sub) next_start = g.start_stage(next_record, p.v2);
+      }
+    }
+    __syncwarp();
+
+    if (p.sigma) {
+#pragma unroll
+      for (int r = 0; r < NPL; ++r) {
+        const int j = r * 32 + lane;
+        if (!valid[r]) continue;
+        if constexpr (std::is_integral<M>::value) {
+          static_cast<std::int64_t*>(p.sigma)[(m - p.frame_begin) * S + j] = static_cast<std::int64_t>(sig[r]) + offset;
+        } else {
+          static_cast<double*>(p.sigma)[(m - p.frame_begin) * S + j] = sig[r];
+        }
+      }
+    }
+
+    // Parallel traceback (decoder.cpp:214-236): lane owns subframes s = lane mod 32.
+    // The decision words of 4 stages are loaded before the state chain walks
+    // them, so the chain is select + shift instead of a load per stage.
+    const std::uint32_t lmask = static_cast<std::uint32_t>(S / 2 - 1);
+    for (std::int64_t s = lane; s < g.num_sub; s += 32) {
+      const std::int64_t st = g.start_stage(s, p.v2);
+      const std::int64_t lo = g.sub_lo(s), hi = g.sub_hi(s);
+      std::uint32_t state;
+      if (p.f0 > 0 && p.start == 1 && st < len - 1) {
+        state = static_cast<std::uint32_t>(mix_seed(p.seed, static_cast<std::uint64_t>(m) * 0x10001ull +
+                                                                static_cast<std::uint64_t>(s)) %
+                                           static_cast<std::uint64_t>(S));
+      } else {
+        state = static_cast<std::uint32_t>(start_state[s]);
+      }
+      std::uint32_t acc = 0;
+      std::int64_t cur = -1;
+      const std::int64_t tend = lo - g.beg;
+      auto step_one = [&](std::int64_t t, std::uint32_t word) {
+        const std::int64_t stage = g.beg + t;
+        if (stage < hi) {
+          const std::int64_t rel = stage - p.out_stage0;
+          const std::int64_t w = rel >> 5;
+          if (w != cur) {
+            if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+            cur = w;
+            acc = 0;
+          }
+          acc |= (state >> (p.k - 2)) << (rel & 31);
+        }
+        state = ((state & lmask) << 1) | ((word >> (state & 31)) & 1u);
+      };
+      std::int64_t t = st;
+      for (; t - 3 >= tend; t -= 4) {
+        std::uint32_t wv[4][NPL];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+#pragma unroll
+          for (int r = 0; r < NPL; ++r) wv[u][r] = dec[(t - u) * NPL + r];
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          std::uint32_t word = wv[u][0];
+#pragma unroll
+          for (int r = 1; r < NPL; ++r) word = (state >> 5) == static_cast<std::uint32_t>(r) ? wv[u][r] : word;
+          step_one(t - u, word);
+        }
+      }
+      for (; t >= tend; --t) step_one(t, dec[t * NPL + (state >> 5)]);
+      if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+    }
+    __syncwarp();
+  }
+}
+
+template <typename In, typename M, int NPL>
+cudaError_t launch_reg(GenericParams gp, cudaStream_t stream) {
+  const DecodeLaunch& p = gp.p;
+  const std::int64_t frames = p.frame_end - p.frame_begin;
+  const std::size_t head = (sizeof(int) * gp.nsub_max + 15) & ~std::size_t(15);
+  const std::size_t stage_bytes = (sizeof(In) * kStage * p.b + 15) & ~std::size_t(15);
+  gp.stage_off = static_cast<int>(head);
+  gp.dec_off = static_cast<int>(head + stage_bytes);
+  const std::size_t dec_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>(gp.len_max) * NPL;
+  constexpr std::size_t kSmemBudget = 200 * 1024;
+  gp.dec_in_smem = (head + stage_bytes + dec_bytes) * kWarps <= kSmemBudget;
+  const std::size_t per_warp = ((gp.dec_in_smem ? head + stage_bytes + dec_bytes : head + stage_bytes) + 15) & ~std::size_t(15);
+  if (per_warp * kWarps > kSmemBudget) return cudaErrorInvalidValue;
+  gp.smem_per_warp = static_cast<int>(per_warp);
+  std::int64_t blocks = (frames + kWarps - 1) / kWarps;
+  const int occ_blocks = sm_count() * 8;
+  if (blocks > occ_blocks) blocks = occ_blocks;
+  gp.dec_global = nullptr;
+  if (!gp.dec_in_smem) {
+    const std::size_t bytes = dec_bytes * static_cast<std::size_t>(blocks) * kWarps;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&gp.dec_global), bytes, stream);
+    if (e != cudaSuccess) return e;
+  }
+  const std::size_t smem = per_warp * kWarps;
+  auto kern = reg_kernel<In, M, NPL>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  if (e == cudaSuccess) {
+    kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(gp);
+    e = cudaGetLastError();
+  }
+  if (gp.dec_global) {
+    const cudaError_t e2 = cudaFreeAsync(gp.dec_global, stream);
+    if (e == cudaSuccess) e = e2;
+  }
+  return e;
+}
+
 template <typename In, typename M>
 cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
   GenericParams gp;
@@ -229,6 +500,15 @@ cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
   const std::int64_t frames = p.frame_end - p.frame_begin;
   if (frames <= 0) return cudaSuccess;
 
+  if (p.s <= 256) {
+    switch (p.s <= 32 ? 1 : p.s / 32) {
+      case 1: return launch_reg<In, M, 1>(gp, stream);
+      case 2: return launch_reg<In, M, 2>(gp, stream);
+      case 4: return launch_reg<In, M, 4>(gp, stream);
+      case 8: return launch_reg<In, M, 8>(gp, stream);
+      default: break;
+    }
+  }
   const std::size_t head = sizeof(M) * (2 * p.s + (1 << p.b)) + sizeof(int) * (gp.nsub_max + (gp.nsub_max & 1));
   const std::size_t head_al = (head + 15) & ~std::size_t(15);
   const std::size_t stage_bytes = (sizeof(In) * kStage * p.b + 15) & ~std::size_t(15);

@@ -231,10 +231,11 @@ def test_error_behaviour_on_gpu():
 
 
 FAST_CODES = [(7, 2, [0o171, 0o133]), (7, 2, [0o133, 0o171]), (9, 2, [0o561, 0o753]), (9, 2, [0o753, 0o561]),
-              (5, 2, [0o23, 0o35]), (6, 2, [0o53, 0o75]), (8, 2, [0o247, 0o371])]
+              (5, 2, [0o23, 0o35]), (6, 2, [0o53, 0o75]), (8, 2, [0o247, 0o371]),
+              (7, 3, [0o133, 0o171, 0o165])]
 
 
-@pytest.mark.parametrize("code", FAST_CODES, ids=lambda c: f"K{c[0]}_{c[2][0]:o}")
+@pytest.mark.parametrize("code", FAST_CODES, ids=lambda c: f"K{c[0]}B{c[1]}_{c[2][0]:o}")
 def test_fast_path_vs_oracle(code, port):
     """The register-resident kernel (interior frames) + generic kernel (edge
     frames) against the oracle over many frame configurations."""
@@ -262,7 +263,7 @@ def test_fast_path_metrics(port):
 
     from paper_2011_09337_b200.device import decode_i8_device
 
-    for k, b, polys in [K7, (9, 2, [0o561, 0o753])]:
+    for k, b, polys in [K7, (9, 2, [0o561, 0o753]), (7, 3, [0o133, 0o171, 0o165])]:
         n = 50_000
         rx, _ = port.gen_bench_block(k, b, polys, n, 2.0, 3)
         q = oracle.quantize(rx, 32.0)
@@ -278,3 +279,21 @@ def test_fast_path_metrics(port):
             got = sigma.cpu().numpy().astype(np.float64)
             bad = np.flatnonzero(np.any(got != sig, axis=1))
             assert bad.size == 0, (k, cfg, bad[:5])
+
+
+@pytest.mark.parametrize("code", [(7, 2, [0o171, 0o133]), (7, 3, [0o133, 0o171, 0o165]), (9, 2, [0o561, 0o753])],
+                         ids=lambda c: f"K{c[0]}B{c[1]}")
+def test_fast_path_full_int8_range(code, port):
+    """Every int8 value, -128 included (outside the quantiser's range but legal
+    input): the fast kernel's offset-binary negation must stay exact."""
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng(99 + k + b)
+    n = 40_000
+    q = rng.integers(-128, 128, n * b).astype(np.int8)
+    q[rng.random(n * b) < 0.2] = -128
+    for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 44, 32)):
+        exp, _, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        packed, _ = vd.framed_decode_stream(q, n, t, cfg)
+        got = vd.unpack_bits(packed, n)
+        assert np.array_equal(got, exp), (code, cfg, np.flatnonzero(got != exp)[:10])
