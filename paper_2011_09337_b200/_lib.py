@@ -12,7 +12,8 @@ import os
 import threading
 from pathlib import Path
 
-LIB_PATH = Path(__file__).resolve().with_name("libvitdec_b200.so")
+# VITDEC_LIB selects another build of the same library (kernel tuning A/B runs).
+LIB_PATH = Path(os.environ.get("VITDEC_LIB") or Path(__file__).resolve().with_name("libvitdec_b200.so"))
 
 VD_OK, VD_EINVAL, VD_ECUDA, VD_EUNSUPPORTED, VD_ENOMEM = 0, 1, 2, 3, 4
 

@@ -141,8 +141,50 @@ struct Geo {
     }
     return best;
   }
-  static constexpr int LSTRIDE = pick_strides().l;
-  static constexpr int XSTRIDE = pick_strides().x;
+  // Chunked relayout (CS = 2^(r-g) >= 4 consecutive registers of an old lane
+  // land in one new lane): one STS.128 and one LDS.128 per 4 registers.
+  // Chunk (a, lam) = old lane lam's registers a*CS .. a*CS+CS-1, read by new
+  // lane a, at word a * AS + lam * CS of the group's area (group pitch XS).
+  static constexpr int CS = (g <= r) ? (1 << (r - g)) : 0;
+  static constexpr bool kChunked = g > 0 && CS >= 4;
+  static constexpr int chunk_cost(int as, int xs) {
+    int cost = 0;
+    for (int side = 0; side < 2; ++side) {        // 0: writes (fixed a), 1: reads (fixed lam)
+      for (int fix = 0; fix < G; ++fix) {
+        for (int part = 0; part < CS / 4; ++part) {
+          for (int h = 0; h < 4; ++h) {             // quarter-warps: 8 lanes x 16 B
+            int cnt[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+            for (int ln = 8 * h; ln < 8 * h + 8; ++ln) {
+              const int gq = ln / G, lm = ln % G;
+              const int a = side == 0 ? fix : lm, l2 = side == 0 ? lm : fix;
+              const int addr = gq * xs + a * as + l2 * CS + 4 * part;
+              cnt[(addr / 4) % 8] += 1;
+            }
+            int wq = 0;
+            for (int b = 0; b < 8; ++b) wq = cnt[b] > wq ? cnt[b] : wq;
+            cost += wq;
+          }
+        }
+      }
+    }
+    return cost;
+  }
+  static constexpr Strides pick_chunk_strides() {
+    Strides best{R, G * R};
+    int bc = 1 << 30;
+    for (int as = R; as < R + 64; as += 4) {
+      for (int xs = G * as; xs < G * as + 64; xs += 4) {
+        const int c = chunk_cost(as, xs) * 4096 + xs;
+        if (c < bc) {
+          bc = c;
+          best = Strides{as, xs};
+        }
+      }
+    }
+    return best;
+  }
+  static constexpr int LSTRIDE = kChunked ? pick_chunk_strides().l : pick_strides().l;  // AS when chunked
+  static constexpr int XSTRIDE = kChunked ? pick_chunk_strides().x : pick_strides().x;
   static_assert(R <= S && R >= 4 && (R & (R - 1)) == 0, "R must be a power of two in [4, S]");
   static_assert(G <= 32, "at most one frame pair per 32 lanes");
   static_assert(R % 4 == 0, "relayout reads use 128-bit loads");
@@ -204,6 +246,21 @@ __device__ __forceinline__ std::uint32_t ldg_pinned(const std::uint32_t* p) {
   return v;
 }
 
+// a * b + c as an IMAD on the FMA pipe (b is an opaque register, so ptxas
+// cannot strength-reduce it into an ALU-pipe add or shift).
+__device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
+  std::uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+
+#ifndef VD_FMA_PAIRS
+#define VD_FMA_PAIRS 4
+#endif
+// Butterflies per stage whose decision words use the FMA-pipe form (balances
+// the ALU and FMA pipes; the rest use the one-instruction ALU form).
+constexpr int kFmaPairs = VD_FMA_PAIRS;
+
 // (a & m) | (b & ~m) as one LOP3 that the compiler cannot re-associate into a
 // serial chain (keeps the decision-compaction tree 3 deep).
 template <std::uint32_t MASK>
@@ -244,6 +301,7 @@ struct FrameState {
   std::uint32_t fw[GEO::WPB];
   std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : 3];
   std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
+  std::uint32_t one, two, m1;         // opaque 1, 2, -1 (IMAD multipliers)
 };
 
 // Branch tables of one block: PT[k][x] = T_k[x ^ lane part] + 128 B per half
@@ -291,6 +349,11 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
 __device__ __forceinline__ void tmem_st1(std::uint32_t taddr, std::uint32_t v) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
 }
+__device__ __forceinline__ void tmem_st4(std::uint32_t taddr, const std::uint32_t (&v)[4]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(taddr), "r"(v[0]), "r"(v[1]),
+               "r"(v[2]), "r"(v[3])
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld4(std::uint32_t taddr, std::uint32_t (&v)[4]) {
   asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
                : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
@@ -331,6 +394,15 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   // ---- branch-metric tables for the LB stages of this block (both frames) ---
   std::uint32_t PT[LB][1 << GEO::B];
   block_tables<C, GEO, BUF>(st, PT);
+  // Decision-word tables of the FMA-pipe form (see the ACS below):
+  // CN[k][x] = PT[x] - PT[x ^ XM] + 0x7FFF per half = 2 PT[x] - OFFB + 0x7FFF7FFF.
+  constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * GEO::B) * 0x00010001u;
+  std::uint32_t CN[LB][1 << GEO::B];
+#pragma unroll
+  for (int k = 0; k < LB; ++k) {
+#pragma unroll
+    for (int x = 0; x < (1 << GEO::B); ++x) CN[k][x] = mad_u32(PT[k][x], st.two, 0x7fff7fffu - OFFB);
+  }
   // The words of this buffer are consumed: refill it with block blk + 2 now,
   // so two full blocks of work cover the HBM latency.
   // pf_room = words left in the frame window from pf: near the window end the
@@ -351,11 +423,13 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       st.llr[BUF][1][i] = ldg_pinned(pfB + o);
     }
   }
+  std::uint32_t tw[4];
 #pragma unroll
   for (int k = 0; k < LB; ++k) {
     const int t = blk * LB + k;
     std::uint32_t* w = st.wv[k & 1];
     // ---- add-compare-select, in place: E/O registers differ in bit k -------
+    int pair = 0;
 #pragma unroll
     for (int e = 0; e < R; ++e) {
       if ((e >> k) & 1) continue;
@@ -366,13 +440,22 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       const std::uint32_t s2H = __vadd2(sO, PT[k][x]);
       const std::uint32_t nL = __viaddmax_s16x2(sE, PT[k][x], s2L);
       const std::uint32_t nH = __viaddmax_s16x2(sE, PT[k][x ^ XM], s2H);
-      // new - second candidate >= 0 per half, 0 iff the second predecessor
-      // won (ties included, decoder.cpp:67-74); + 0x7FFF per half moves
-      // "nonzero" into bit 15 / 31 without a carry between the halves.
-      w[e] = nL - s2L + 0x7fff7fffu;
-      w[od] = nH - s2H + 0x7fff7fffu;
+      // Decision words: bit 15 / 31 set iff the FIRST predecessor won, i.e.
+      // s1 - s2 >= 1 per half (ties -> second, decoder.cpp:67-74); + 0x7FFF
+      // per half keeps each half in [0, 0xFFFE], so no carry crosses halves.
+      if (pair < kFmaPairs) {
+        // FMA-pipe form: (sE - sO) + (PT[x] - PT[x ^ XM] + 0x7FFF), 3 IMAD per pair
+        const std::uint32_t d = mad_u32(sO, st.m1, sE);
+        w[e] = mad_u32(d, st.one, CN[k][x]);
+        w[od] = mad_u32(d, st.one, CN[k][x ^ XM]);
+      } else {
+        // ALU-pipe form: new - s2 (>= 0, 0 iff the second won) + 0x7FFF, 1 IADD3 each
+        w[e] = nL - s2L + 0x7fff7fffu;
+        w[od] = nH - s2H + 0x7fff7fffu;
+      }
       st.sig[e] = nL;
       st.sig[od] = nH;
+      ++pair;
     }
     // ---- previous stage's decisions -> survivor store (overlaps this ACS) --
     const std::uint32_t word = compact16(st.wv[(k + 1) & 1]);
@@ -383,9 +466,10 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     } else if constexpr (MODE == 1) {
       bc.drow_lane[(t - 1 - bc.s_base) * 32] = word;
     } else {
-      tmem_st1(bc.taddr + static_cast<std::uint32_t>(t - 1 - bc.t_first), word);
+      tw[k] = word;  // one 4-column tensor-memory store per block, below
     }
   }
+  if constexpr (MODE == 2) tmem_st4(bc.taddr + static_cast<std::uint32_t>(blk * LB - 1 - bc.t_first), tw);
   if constexpr (MODE != 0) tprev = blk * LB + LB - 1;
 }
 
@@ -477,6 +561,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
 #pragma unroll
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
   }
+  st.one = opaque(1u);
+  st.two = opaque(2u);
+  st.m1 = opaque(0xffffffffu);
 #pragma unroll
   for (int i = 0; i < R; ++i) st.sig[i] = BASE;
 #pragma unroll
@@ -567,6 +654,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
 
   // (opaque offset, not pointer: the accesses must stay STS/LDS)
   std::uint32_t* const xb = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE));
+  // chunked relayout: this lane writes its chunks at lam * CS, reads its own at lam * AS
+  std::uint32_t* const xw = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE + lam * GEO::CS));
+  const std::uint32_t* const xr = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE + lam * GEO::LSTRIDE));
   auto block_end = [&](int blk) {
     // ---- renormalisation every 4 blocks (group-wide reference): metrics stay
     // within [BASE - spread, BASE + spread + 16 * 510] (< 32768 up to K = 9).
@@ -578,7 +668,32 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
       for (int i = 0; i < R; ++i) st.sig[i] = st.sig[i] - ref + BASE;
     }
     // ---- relayout: back to the canonical layout (P_new = rotr(P_old, r)) --
-    if constexpr (g > 0) {
+    if constexpr (GEO::kChunked) {
+      constexpr int CS = GEO::CS, AS = GEO::LSTRIDE;
+#pragma unroll
+      for (int a = 0; a < G; ++a) {
+#pragma unroll
+        for (int q = 0; q < CS / 4; ++q) {
+          const int i = a * CS + 4 * q;
+          *reinterpret_cast<uint4*>(xw + a * AS + 4 * q) =
+              make_uint4(st.sig[i], st.sig[i + 1], st.sig[i + 2], st.sig[i + 3]);
+        }
+      }
+      __syncwarp();
+#pragma unroll
+      for (int l2 = 0; l2 < G; ++l2) {
+#pragma unroll
+        for (int q = 0; q < CS / 4; ++q) {
+          const uint4 v = *reinterpret_cast<const uint4*>(xr + l2 * CS + 4 * q);
+          // old register a*CS + c of old lane l2 -> new register (c << g) | l2
+          st.sig[((4 * q + 0) << g) | l2] = v.x;
+          st.sig[((4 * q + 1) << g) | l2] = v.y;
+          st.sig[((4 * q + 2) << g) | l2] = v.z;
+          st.sig[((4 * q + 3) << g) | l2] = v.w;
+        }
+      }
+      __syncwarp();
+    } else if constexpr (g > 0) {
 #pragma unroll
       for (int i = 0; i < R; ++i) {
         // old (lam, i) -> new physical index rotr(lam * R + i, r) = (i << g) | lam
@@ -696,16 +811,16 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
         std::uint32_t own[4];
         tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
 #pragma unroll
-        for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp)) >> hsh;
+        for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
       } else {
 #pragma unroll
         for (int j = 0; j < LB; ++j) {
           const int row = max(tb0 + j - s_base, 0);
-          wd[j] = dec[row * 32 + gcol + lp] >> hsh;
+          wd[j] = dec[row * 32 + gcol + lp];
         }
       }
       const std::uint32_t Pin = P;
-      std::uint32_t u = P & (R - 1);
+      std::uint32_t u = (P & (R - 1)) | hsh;  // bit index into the word: register + 16 * half
       if (tb0 + LB - 1 <= st_min && tb0 >= lo_max) {
         // every task walks all LB phases of this block
 #pragma unroll
@@ -713,7 +828,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
           const std::uint32_t dbit = (wd[j] >> u) & 1u;
           u = (u & ~(1u << j)) | (dbit << j);
         }
-        P = (P & ~static_cast<std::uint32_t>(R - 1)) | u;
+        P = (P & ~static_cast<std::uint32_t>(R - 1)) | (u & (R - 1));
         if (tb0 + LB - 1 < hi_min) {
           emit(tb0, 0, LB, Pin & ((1u << LB) - 1u));
         } else if (tb0 < hi_max) {
@@ -730,7 +845,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
           const std::uint32_t un = (u & ~(1u << j)) | (dbit << j);
           u = (j <= jhi && j >= jlo) ? un : u;
         }
-        P = (P & ~static_cast<std::uint32_t>(R - 1)) | u;
+        P = (P & ~static_cast<std::uint32_t>(R - 1)) | (u & (R - 1));
         const int ejhi = min(min(jhi, sub_hi - 1 - tb0), LB - 1);
         if (ejhi >= jlo) emit(tb0, jlo, ejhi - jlo + 1, (Pin >> jlo) & ((1u << (ejhi - jlo + 1)) - 1u));
         if (tb0 >= sub_lo && tb0 <= st_t) P = ((P << r) | (P >> (M - r))) & GEO::SMASK;  // undo the relayout
