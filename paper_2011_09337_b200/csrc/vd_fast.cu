@@ -255,11 +255,14 @@ __device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t 
 }
 
 #ifndef VD_FMA_PAIRS
-#define VD_FMA_PAIRS 4
+#define VD_FMA_PAIRS 6
 #endif
 // Butterflies per stage whose decision words use the FMA-pipe form (balances
 // the ALU and FMA pipes; the rest use the one-instruction ALU form).
 constexpr int kFmaPairs = VD_FMA_PAIRS;
+#ifndef VD_RENORM_EVERY
+#define VD_RENORM_EVERY 2
+#endif
 
 // (a & m) | (b & ~m) as one LOP3 that the compiler cannot re-associate into a
 // serial chain (keeps the decision-compaction tree 3 deep).
@@ -384,7 +387,8 @@ __device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32
 
 // One block of LB stages. MODE 0 (slow) range-checks every pending store and
 // calls the stored-max argmax hook; MODE 1 / 2 are straight-line blocks whose
-// pending stores all go to shared memory / tensor memory.
+// pending stores all go to shared memory / tensor memory; MODE 3 blocks lie
+// entirely in the v1 warm-up (ACS only: no decision words, no stores).
 template <class C, class GEO, int MODE, bool TM, int BUF, class RecFn>
 __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
                                           const std::uint32_t* pfA, const std::uint32_t* pfB, int pf_room,
@@ -443,7 +447,10 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       // Decision words: bit 15 / 31 set iff the FIRST predecessor won, i.e.
       // s1 - s2 >= 1 per half (ties -> second, decoder.cpp:67-74); + 0x7FFF
       // per half keeps each half in [0, 0xFFFE], so no carry crosses halves.
-      if (pair < kFmaPairs) {
+      // (MODE 3: warm-up stages t < v1 keep no decisions, decoder.cpp:229-235
+      // never reads them.)
+      if constexpr (MODE == 3) {
+      } else if (pair < kFmaPairs) {
         // FMA-pipe form: (sE - sO) + (PT[x] - PT[x ^ XM] + 0x7FFF), 3 IMAD per pair
         const std::uint32_t d = mad_u32(sO, st.m1, sE);
         w[e] = mad_u32(d, st.one, CN[k][x]);
@@ -458,6 +465,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       ++pair;
     }
     // ---- previous stage's decisions -> survivor store (overlaps this ACS) --
+    if constexpr (MODE == 3) continue;
     const std::uint32_t word = compact16(st.wv[(k + 1) & 1]);
     if constexpr (MODE == 0) {
       store_dec<TM>(bc, tprev, word);
@@ -657,10 +665,13 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   // chunked relayout: this lane writes its chunks at lam * CS, reads its own at lam * AS
   std::uint32_t* const xw = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE + lam * GEO::CS));
   const std::uint32_t* const xr = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE + lam * GEO::LSTRIDE));
-  auto block_end = [&](int blk) {
-    // ---- renormalisation every 4 blocks (group-wide reference): metrics stay
-    // within [BASE - spread, BASE + spread + 16 * 510] (< 32768 up to K = 9).
-    if ((blk & 3) == 3) {
+  auto block_end = [&](int blk, auto buf_tag) {
+    // ---- renormalisation every 2 blocks (after each odd block: a compile-time
+    // position in the 2-block loop body) or every 4 blocks (group-wide
+    // reference): metrics stay within [BASE - spread, BASE + spread + 16 * 510]
+    // (< 32768 up to K = 9).
+    constexpr int BUFE = decltype(buf_tag)::value;
+    if (VD_RENORM_EVERY == 2 ? BUFE == 1 : (blk & 3) == 3) {
       const std::uint32_t ref = __shfl_sync(kFull, st.sig[0], grp * G);
       subA += static_cast<std::int32_t>(ref & 0xffffu) - 8192;
       subB += static_cast<std::int32_t>(ref >> 16) - 8192;
@@ -720,7 +731,10 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     // Straight-line block: pending stores (stages t0-1 .. t0+LB-2) all inside
     // [v1, L) and on one side of the TMEM/smem split, no start stage inside.
     const bool clean = (t0 - 1 >= v1) && (t0 + LB - 2 < L) && !(next_rec >= t0 && next_rec < t0 + LB);
-    if (clean && t0 - 1 >= t_split) {
+    if (t0 + LB <= v1) {
+      // warm-up block: every stage (and the next block's pending one) < v1
+      run_block<C, GEO, 3, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+    } else if (clean && t0 - 1 >= t_split) {
       run_block<C, GEO, 1, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     } else if (TM && clean && t0 + LB - 2 < t_split) {
       run_block<C, GEO, 2, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
@@ -730,7 +744,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     pf_off += WPB;
     pfA += WPB;
     pfB += WPB;
-    block_end(blk);
+    block_end(blk, buf_tag);
   };
   for (int blk = 0; blk < nblk; blk += 2) {
     one_block(blk, std::integral_constant<int, 0>{});
