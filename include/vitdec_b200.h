@@ -132,6 +132,31 @@ vd_status vd_decode_f64_device(const vd_code* code, const vd_frame_cfg* cfg, int
 vd_status vd_frame_window(const vd_frame_cfg* cfg, int64_t n_stages, int64_t frame_begin, int64_t frame_end,
                           int64_t* begin, int64_t* end);
 
+/* ---- batched independent blocks ------------------------------------------ */
+
+/* Decodes n_blocks independent LLR blocks in one device pass, each exactly as
+ * its own framed_decode call would (reference decoder.hpp:74-79): its own
+ * frame grid, frames clipped at both ends of the block, random-start salt
+ * from the block-local frame index. This is how reference run_ber_sweep
+ * decodes a BER point (berlab.cpp:63-88: one framed_decode per block of
+ * block_bits). Block j holds block_stages[j] >= 1 stages (host array); the
+ * blocks are concatenated in llr_dev, and block j's decoded bits land in
+ * out_dev at bit offset block_stages[0] + ... + block_stages[j-1] (the whole
+ * ceil(total/32)-word range is overwritten). stats (may be NULL) is the sum
+ * over blocks. Asynchronous with respect to the host. */
+vd_status vd_decode_batch_i8_device(const vd_code* code, const vd_frame_cfg* cfg, int32_t n_blocks,
+                                    const int64_t* block_stages, const int8_t* llr_dev, uint32_t* out_dev,
+                                    vd_stats* stats, int32_t device, void* stream);
+vd_status vd_decode_batch_f64_device(const vd_code* code, const vd_frame_cfg* cfg, int32_t n_blocks,
+                                     const int64_t* block_stages, const double* llr_dev, uint32_t* out_dev,
+                                     vd_stats* stats, int32_t device, void* stream);
+/* Host-buffer form (one device: exec->devices[0], or the current device):
+ * H2D of the concatenated blocks, the batched decode, D2H of the packed bits.
+ * Synchronous. */
+vd_status vd_decode_batch_i8(const vd_code* code, const vd_frame_cfg* cfg, int32_t n_blocks,
+                             const int64_t* block_stages, const int8_t* llr, uint32_t* out_packed, vd_stats* stats,
+                             const vd_exec* exec);
+
 /* ---- host-buffer decode: the reference-facing call ------------------------ */
 
 /* framed_decode (reference decoder.hpp:74-79) on host buffers: streams the

@@ -17,6 +17,7 @@ from .api import (
     frame_stats,
     frame_window,
     framed_decode,
+    framed_decode_batch,
     framed_decode_stream,
     pack_bits,
     partition_frames,
@@ -38,6 +39,7 @@ __all__ = [
     "frame_stats",
     "frame_window",
     "framed_decode",
+    "framed_decode_batch",
     "framed_decode_stream",
     "pack_bits",
     "partition_frames",

@@ -59,6 +59,9 @@ SIGNATURES = {
     "vd_decode_i8_device": (I32, [P, C.POINTER(VdFrameCfg), I64, P, I64, I64, I64, P, I64, P, I32, P]),
     "vd_decode_f64_device": (I32, [P, C.POINTER(VdFrameCfg), I64, P, I64, I64, I64, P, I64, P, I32, P]),
     "vd_frame_window": (I32, [C.POINTER(VdFrameCfg), I64, I64, I64, C.POINTER(I64), C.POINTER(I64)]),
+    "vd_decode_batch_i8_device": (I32, [P, C.POINTER(VdFrameCfg), I32, P, P, P, C.POINTER(VdStats), I32, P]),
+    "vd_decode_batch_f64_device": (I32, [P, C.POINTER(VdFrameCfg), I32, P, P, P, C.POINTER(VdStats), I32, P]),
+    "vd_decode_batch_i8": (I32, [P, C.POINTER(VdFrameCfg), I32, P, P, P, C.POINTER(VdStats), C.POINTER(VdExec)]),
     "vd_decode_i8": (I32, [P, C.POINTER(VdFrameCfg), P, I64, P, C.POINTER(VdStats), C.POINTER(VdExec)]),
     "vd_decode_f64": (I32, [P, C.POINTER(VdFrameCfg), P, I64, P, C.POINTER(VdStats), C.POINTER(VdExec)]),
     "vd_serial_decode_f64": (I32, [P, P, I64, P, C.POINTER(VdStats), I32]),

@@ -261,6 +261,45 @@ def framed_decode(llr: np.ndarray, trellis: Trellis, cfg: FrameConfig, workers: 
     return DecodeOutput(unpack_bits(packed, n), st)
 
 
+def framed_decode_batch(blocks, trellis: Trellis, cfg: FrameConfig, gpu: int = -1) -> list:
+    """Independent framed decodes of several int8 blocks in one device pass
+    (vd_decode_batch_i8): ``blocks`` is a list of stage-major int8 streams
+    (n_j * B values each) or of B x n_j LlrBlocks. Equivalent to calling
+    framed_decode on every block (reference run_ber_sweep, berlab.cpp:63-88).
+    Returns [(bits uint8[n_j], DecodeStats)] with per-block stats."""
+    b = trellis.outputs_per_bit()
+    streams = []
+    for blk in blocks:
+        a = np.asarray(blk)
+        if a.ndim == 2:
+            _check_block(a, trellis)
+            a = _as_stream(a)
+        if a.dtype != np.int8:
+            raise TypeError("batched decode takes int8 LLR blocks")
+        if a.size == 0 or a.size % b:
+            raise ValueError("empty llr block" if a.size == 0 else "stream length is not n * B")
+        streams.append(np.ascontiguousarray(a).reshape(-1))
+    if not streams:
+        raise ValueError("batch needs at least one block")
+    cfg.validate()
+    lens = np.array([s.size // b for s in streams], np.int64)
+    cat = np.concatenate(streams)
+    total = int(lens.sum())
+    out = np.zeros((total + 31) // 32, np.uint32)
+    st = VdStats()
+    c = cfg.to_c()
+    dev = C.c_int32(int(gpu))
+    ex = VdExec(1, C.pointer(dev), 0) if gpu >= 0 else VdExec(0, None, 0)
+    check(lib().vd_decode_batch_i8(trellis.handle, C.byref(c), len(streams), lens.ctypes.data, cat.ctypes.data,
+                                   out.ctypes.data, C.byref(st), C.byref(ex)))
+    bits = unpack_bits(out, total)
+    res, off = [], 0
+    for n in lens:
+        res.append((bits[off:off + n], frame_stats(cfg, int(n))))
+        off += int(n)
+    return res
+
+
 def serial_decode(llr: np.ndarray, trellis: Trellis) -> DecodeOutput:
     """reference decoder.cpp:101-129 (one frame, no overlap, on the GPU)."""
     llr = np.asarray(llr)

@@ -216,6 +216,160 @@ vd_status decode_device(const vd_code* code, const vd_frame_cfg* cfg, std::int64
   return VD_OK;
 }
 
+// ---- batched independent blocks -------------------------------------------
+// Every block runs its own framed decode (own frame grid, clipped at both of
+// its ends, block-local random-start salt), as reference run_ber_sweep calls
+// framed_decode once per block (berlab.cpp:63-88) — but all blocks go to the
+// device in one fast-kernel launch plus one generic launch for the clipped
+// edge frames of every block.
+
+void batch_stats(const vd_frame_cfg* cfg, std::int32_t nblocks, const std::int64_t* lens, vd_stats* st) {
+  st->frames = st->stages = st->tracebacks = 0;
+  for (std::int32_t j = 0; j < nblocks; ++j) {
+    vd_stats b{};
+    vd_frame_stats(cfg, lens[j], &b);
+    st->frames += b.frames;
+    st->stages += b.stages;
+    st->tracebacks += b.tracebacks;
+  }
+}
+
+template <typename T>
+vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std::int32_t nblocks,
+                              const std::int64_t* lens, const T* llr, std::uint32_t* out, vd_stats* stats,
+                              std::int32_t device, void* stream) {
+  if (!code) return fail(VD_EINVAL, "null code");
+  if (vd_status st = validate_cfg(cfg, 1)) return st;
+  if (nblocks < 1 || !lens) return fail(VD_EINVAL, "batch needs at least one block");
+  for (std::int32_t j = 0; j < nblocks; ++j) {
+    if (lens[j] < 1) return fail(VD_EINVAL, "empty llr block");  // reference decoder.cpp:92-97
+  }
+  if (vd_status st = check_gpu_envelope(code)) return st;
+  if (!llr || !out) return fail(VD_EINVAL, "null buffer");
+  if (stats) batch_stats(cfg, nblocks, lens, stats);
+
+  // Block tables: stage and frame prefixes, fast-kernel interior range per
+  // block, and the list of remaining (edge) frames.
+  const int f = cfg->f, v1 = cfg->v1, v2 = cfg->v2, B = code->b;
+  const std::int64_t L = static_cast<std::int64_t>(f) + v1 + v2;
+  std::vector<std::int64_t> bstage(nblocks + 1, 0), bframe(nblocks + 1, 0);
+  for (std::int32_t j = 0; j < nblocks; ++j) {
+    bstage[j + 1] = bstage[j] + lens[j];
+    bframe[j + 1] = bframe[j] + num_frames(cfg, lens[j]);
+  }
+  const std::int64_t n_total = bstage[nblocks], nf_total = bframe[nblocks];
+
+  vd::DecodeLaunch p;
+  p.k = code->k;
+  p.b = code->b;
+  p.s = code->s;
+  p.f = f;
+  p.v1 = v1;
+  p.v2 = v2;
+  p.f0 = cfg->f0;
+  p.start = cfg->start;
+  p.seed = cfg->seed;
+  p.n = n_total;
+  p.llr = llr;
+  p.out = out;
+  for (int i = 0; i < code->b && i < 8; ++i) p.polys[i] = code->polys[i];
+  p.complement_paired = code->complement_paired;
+  // Does the fast kernel take this code/config at all? (probe on one long stream)
+  bool fast = false;
+  if constexpr (sizeof(T) == 1) {
+    vd::DecodeLaunch probe = p;
+    probe.n = std::max<std::int64_t>(n_total, 64 * L);
+    probe.frame_begin = 0;
+    probe.frame_end = num_frames(cfg, probe.n);
+    fast = vd::fast_path_supported(probe);
+  }
+  std::vector<std::int32_t> ilo(nblocks, 0), ihi(nblocks, 0);
+  std::vector<std::int64_t> edges;
+  std::int64_t safe = -1, interior = 0;
+  for (std::int32_t j = 0; j < nblocks; ++j) {
+    std::int64_t lo = 0, hi = 0;
+    if (fast && (bstage[j] * B) % 4 == 0) {
+      lo = (v1 + f - 1) / f;                                        // m*f >= v1
+      hi = lens[j] - f - v2 >= 0 ? (lens[j] - f - v2) / f + 1 : 0;  // m*f + f + v2 <= n_j
+      // window + 4 stages of prefetch slack inside the whole stream
+      const std::int64_t room = n_total - bstage[j] + v1 - L - 4;
+      hi = std::min(hi, room >= 0 ? room / f + 1 : 0);
+      hi = std::max(hi, lo);
+    }
+    ilo[j] = static_cast<std::int32_t>(lo);
+    ihi[j] = static_cast<std::int32_t>(hi);
+    if (hi > lo && safe < 0) safe = bstage[j] + lo * f - v1;
+    interior += hi - lo;
+    for (std::int64_t m = 0; m < bframe[j + 1] - bframe[j]; ++m) {
+      if (m < lo || m >= hi) edges.push_back(bframe[j] + m);
+    }
+  }
+
+  int dev = 0;
+  if (vd_status st = resolve_device(device, &dev)) return st;
+  DeviceGuard guard(dev);
+  const std::uint32_t* in_out = nullptr;
+  if (vd_status st = device_table(code, dev, &in_out)) return st;
+  p.in_out = in_out;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+
+  // Stream-ordered scratch for the tables (freed after the launches).
+  const std::size_t nb1 = static_cast<std::size_t>(nblocks) + 1;
+  const std::size_t bytes = sizeof(std::int64_t) * (2 * nb1 + edges.size()) + sizeof(std::int32_t) * 2 * nb1;
+  std::vector<unsigned char> host(bytes);
+  std::memcpy(host.data(), bstage.data(), sizeof(std::int64_t) * nb1);
+  std::memcpy(host.data() + sizeof(std::int64_t) * nb1, bframe.data(), sizeof(std::int64_t) * nb1);
+  std::memcpy(host.data() + sizeof(std::int64_t) * 2 * nb1, edges.data(), sizeof(std::int64_t) * edges.size());
+  const std::size_t i32_off = sizeof(std::int64_t) * (2 * nb1 + edges.size());
+  std::memcpy(host.data() + i32_off, ilo.data(), sizeof(std::int32_t) * nblocks);
+  std::memcpy(host.data() + i32_off + sizeof(std::int32_t) * nb1, ihi.data(), sizeof(std::int32_t) * nblocks);
+  unsigned char* dscratch = nullptr;
+  VD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dscratch), bytes, s), "cudaMallocAsync(batch tables)");
+  VD_CUDA(cudaMemcpyAsync(dscratch, host.data(), bytes, cudaMemcpyHostToDevice, s), "upload batch tables");
+  p.nblocks = nblocks;
+  p.blk_stage = reinterpret_cast<const std::int64_t*>(dscratch);
+  p.blk_frame = p.blk_stage + nb1;
+  p.blk_ilo = reinterpret_cast<const std::int32_t*>(dscratch + i32_off);
+  p.blk_ihi = p.blk_ilo + nb1;
+  const std::int64_t* dedges = p.blk_stage + 2 * nb1;
+
+  VD_CUDA(cudaMemsetAsync(out, 0, sizeof(std::uint32_t) * ((n_total + 31) / 32), s), "zero output");
+  cudaError_t e = cudaSuccess;
+  bool fast_launched = false;
+  if (fast && interior > 0) {
+    vd::DecodeLaunch q = p;
+    q.frame_begin = 0;
+    q.frame_end = nf_total;
+    q.safe_stage = safe;
+    if (vd::fast_path_supported(q)) {
+      e = vd::launch_fast_i8(q, s);
+      fast_launched = true;
+    }
+  }
+  if (e == cudaSuccess) {
+    vd::DecodeLaunch q = p;
+    q.frame_begin = 0;
+    if (fast_launched) {
+      q.frame_list = dedges;
+      q.frame_end = static_cast<std::int64_t>(edges.size());
+    } else {
+      q.frame_end = nf_total;
+    }
+    if (q.frame_end > 0) {
+      if constexpr (sizeof(T) == 1) {
+        e = vd::launch_generic_i8(q, s);
+      } else {
+        e = vd::launch_generic_f64(q, s);
+      }
+    }
+  }
+  const cudaError_t ef = cudaFreeAsync(dscratch, s);
+  if (e == cudaErrorInvalidValue) return fail(VD_EUNSUPPORTED, "frame configuration exceeds the GPU kernel's shared-memory envelope");
+  if (e != cudaSuccess) return cuda_fail(e, "batched decode launch");
+  if (ef != cudaSuccess) return cuda_fail(ef, "cudaFreeAsync(batch tables)");
+  return VD_OK;
+}
+
 // ---- host-buffer streaming engine ----------------------------------------
 
 struct DevCtx {
@@ -522,6 +676,45 @@ vd_status vd_decode_f64_device(const vd_code* code, const vd_frame_cfg* cfg, int
                                int64_t llr_stage0, int64_t fb, int64_t fe, uint32_t* out, int64_t out_stage0,
                                double* sigma, int32_t device, void* stream) {
   return decode_device<double>(code, cfg, n, llr, llr_stage0, fb, fe, out, out_stage0, sigma, device, stream);
+}
+
+vd_status vd_decode_batch_i8_device(const vd_code* code, const vd_frame_cfg* cfg, int32_t n_blocks,
+                                    const int64_t* block_stages, const int8_t* llr, uint32_t* out, vd_stats* stats,
+                                    int32_t device, void* stream) {
+  return decode_batch_device<std::int8_t>(code, cfg, n_blocks, block_stages, llr, out, stats, device, stream);
+}
+
+vd_status vd_decode_batch_f64_device(const vd_code* code, const vd_frame_cfg* cfg, int32_t n_blocks,
+                                     const int64_t* block_stages, const double* llr, uint32_t* out, vd_stats* stats,
+                                     int32_t device, void* stream) {
+  return decode_batch_device<double>(code, cfg, n_blocks, block_stages, llr, out, stats, device, stream);
+}
+
+vd_status vd_decode_batch_i8(const vd_code* code, const vd_frame_cfg* cfg, int32_t n_blocks,
+                             const int64_t* block_stages, const int8_t* llr, uint32_t* out, vd_stats* stats,
+                             const vd_exec* exec) {
+  if (!code) return fail(VD_EINVAL, "null code");
+  if (n_blocks < 1 || !block_stages) return fail(VD_EINVAL, "batch needs at least one block");
+  std::int64_t n = 0;
+  for (std::int32_t j = 0; j < n_blocks; ++j) n += block_stages[j] > 0 ? block_stages[j] : 0;
+  int dev = 0;
+  if (vd_status st = resolve_device(exec && exec->num_devices > 0 && exec->devices ? exec->devices[0] : -1, &dev))
+    return st;
+  DeviceGuard guard(dev);
+  DevCtx& ctx = tl_ctx.devs[dev];
+  if (!ctx.st[0]) VD_CUDA(cudaStreamCreateWithFlags(&ctx.st[0], cudaStreamNonBlocking), "cudaStreamCreate");
+  const std::size_t words = static_cast<std::size_t>((n + 31) / 32);
+  if (vd_status st = ensure(&ctx.llr[0], &ctx.llr_cap[0], static_cast<std::size_t>(n) * code->b)) return st;
+  if (vd_status st = ensure(reinterpret_cast<void**>(&ctx.out[0]), &ctx.out_cap[0], words * 4)) return st;
+  cudaStream_t s = ctx.st[0];
+  VD_CUDA(cudaMemcpyAsync(ctx.llr[0], llr, static_cast<std::size_t>(n) * code->b, cudaMemcpyHostToDevice, s), "H2D");
+  if (vd_status st = decode_batch_device<std::int8_t>(code, cfg, n_blocks, block_stages,
+                                                      static_cast<const std::int8_t*>(ctx.llr[0]), ctx.out[0], stats,
+                                                      dev, s))
+    return st;
+  VD_CUDA(cudaMemcpyAsync(out, ctx.out[0], words * 4, cudaMemcpyDeviceToHost, s), "D2H");
+  VD_CUDA(cudaStreamSynchronize(s), "batched decode");
+  return VD_OK;
 }
 
 vd_status vd_decode_i8(const vd_code* code, const vd_frame_cfg* cfg, const int8_t* llr, int64_t n, uint32_t* out,

@@ -230,6 +230,7 @@ struct FastParams {
   // (row = t - s_base); row smem_rows - 1 is a dummy sink.
   int t_first, t_split, s_base, smem_rows, tcols;
   int tm_alloc;  // TMEM columns allocated per CTA (power of two)
+  std::int64_t safe_stage;  // window start of an interior frame (loads of empty frame slots)
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -522,8 +523,20 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   const std::int64_t mbase = fp.mi0 + gwarp * GEO::FPW;
   if (mbase < fp.mi1) {  // (no early return: TMEM dealloc needs every warp at the barrier)
   const std::int64_t mA = mbase + 2 * grp, mB = mA + 1;
-  const bool validA = mA < fp.mi1, validB = mB < fp.mi1;
-  const std::int64_t lA = validA ? mA : fp.mi0, lB = validB ? mB : fp.mi0;  // clamp loads
+  bool validA = mA < fp.mi1, validB = mB < fp.mi1;
+  // Window start stage of a frame slot; empty slots (past the launch, or in
+  // batched mode a clipped edge frame of its block) load an interior frame's
+  // LLRs and write nothing.
+  struct Slot {
+    std::int64_t ws, m;  // window start stage (stream), block-local frame index
+  };
+  auto frame_slot = [&](std::int64_t mg, bool& valid) -> Slot {
+    if (!valid) return Slot{fp.safe_stage, 0};
+    const FrameRef r = resolve_frame(p, mg);
+    if (p.nblocks > 0) valid = r.m >= __ldg(p.blk_ilo + r.blk) && r.m < __ldg(p.blk_ihi + r.blk);
+    return valid ? Slot{r.base + r.m * p.f - p.v1, r.m} : Slot{fp.safe_stage, 0};
+  };
+  const std::int64_t wsA = frame_slot(mA, validA).ws, wsB = frame_slot(mB, validB).ws;
 
   const int f = static_cast<int>(opaque(static_cast<std::uint32_t>(p.f)));
   const int v1 = static_cast<int>(opaque(static_cast<std::uint32_t>(p.v1)));
@@ -537,9 +550,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   const int s_base = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.s_base)));
   // Frame-relative LLR word pointers (frame start is 4-byte aligned: checked at launch).
   const std::uint32_t* llrA = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
-                                                                     (lA * f - v1 - p.llr_stage0) * B);
+                                                                     (wsA - p.llr_stage0) * B);
   const std::uint32_t* llrB = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
-                                                                     (lB * f - v1 - p.llr_stage0) * B);
+                                                                     (wsB - p.llr_stage0) * B);
 
   FrameState<GEO> st;
   // Per-phase flip constants for this lane (lane part of the branch index).
@@ -770,8 +783,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     const int fr = active ? task % GEO::FPW : 0;  // frame slot in the warp (2 * group + half)
     const int s = active ? task / GEO::FPW : 0;
     const int half = fr & 1;
-    const std::int64_t m = mbase + fr;
-    const bool valid = active && m < fp.mi1;
+    bool valid = active && mbase + fr < fp.mi1;
+    const Slot sl = frame_slot(mbase + fr, valid);
+    const std::int64_t m = sl.m;  // block-local frame index (random-start salt)
     const int st_t = active ? sub_start(s) : -1;
     const int sub_lo = v1 + s * step;
     const int sub_hi = v1 + min((s + 1) * step, f);
@@ -788,7 +802,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     std::uint32_t P = sh == 0 ? state : (((state << sh) | (state >> (M - sh))) & GEO::SMASK);
     const std::uint32_t hsh = half ? 16u : 0u;
     const int gcol = (fr >> 1) * G;  // this frame's group: first lane of its decision columns
-    const std::int64_t obase = m * f - v1 - p.out_stage0;  // output bit index of frame-relative stage 0
+    const std::int64_t obase = sl.ws - p.out_stage0;  // output bit index of frame-relative stage 0
     std::uint64_t acc = 0;  // emitted bits, newest (lowest stage) at bit 0
     int nb = 0;
     // Round-uniform bounds (inactive lanes have st_t = -1 and sub_lo = v1).
@@ -962,6 +976,14 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   constexpr int B = GEO::B;
   if ((static_cast<std::int64_t>(p.f) * B) % 4 != 0 || (static_cast<std::int64_t>(p.v1) * B) % 4 != 0) return false;
   if ((p.llr_stage0 * B) % 4 != 0) return false;
+  if (p.nblocks > 0) {
+    // Batched: the caller launches every global frame and marks the interior
+    // ones per block (blk_ilo / blk_ihi); edge frames go to the generic kernel.
+    fp.mi0 = p.frame_begin;
+    fp.mi1 = p.frame_end;
+    fp.safe_stage = p.safe_stage;
+    if (p.frame_list || p.sigma) return false;
+  } else {
   const std::int64_t span = static_cast<std::int64_t>(fp.L) + 4;  // stages read per frame (word granularity slack)
   std::int64_t lo = (p.v1 + p.f - 1) / p.f;                                    // first m with m*f >= v1
   std::int64_t hi_excl = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // m*f + f + v2 <= n
@@ -974,6 +996,8 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   if (fp.mi1 - fp.mi0 < GEO::FPW) return false;  // not worth it
   // also the llr window must start at or before the first interior frame's beg
   if (p.llr_stage0 > fp.mi0 * p.f - p.v1) return false;
+  fp.safe_stage = fp.mi0 * p.f - p.v1;
+  }
   const int x_bytes = GEO::g > 0 ? GEO::GROUPS * GEO::XSTRIDE * 4 : 0;
   const int ss_bytes = ((GEO::FPW * fp.num_sub * 2) + 15) & ~15;
   auto layout = [&](int smem_rows) {
@@ -1033,7 +1057,7 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   const FastParams& fp = pl.fp;
   // Edge frames (clipped windows) go to the generic kernel on a side stream,
   // concurrently with the fast kernel (they fit beside its CTA on an SM).
-  const bool edges = fp.mi0 > p.frame_begin || fp.mi1 < p.frame_end;
+  const bool edges = p.nblocks == 0 && (fp.mi0 > p.frame_begin || fp.mi1 < p.frame_end);
   SideStream* side = nullptr;
   if (edges) {
     side = side_stream();
@@ -1041,12 +1065,12 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
     if (cudaError_t err = cudaEventRecord(side->fork, stream); err != cudaSuccess) return err;
     if (cudaError_t err = cudaStreamWaitEvent(side->s, side->fork, 0); err != cudaSuccess) return err;
   }
-  if (fp.mi0 > p.frame_begin) {
+  if (edges && fp.mi0 > p.frame_begin) {
     DecodeLaunch e = p;
     e.frame_end = fp.mi0;
     if (cudaError_t err = launch_generic_i8(e, side->s); err != cudaSuccess) return err;
   }
-  if (fp.mi1 < p.frame_end) {
+  if (edges && fp.mi1 < p.frame_end) {
     DecodeLaunch e = p;
     e.frame_begin = fp.mi1;
     if (p.sigma) e.sigma = static_cast<std::int64_t*>(p.sigma) + (fp.mi1 - p.frame_begin) * p.s;

@@ -79,8 +79,10 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
   const In* llr = static_cast<const In*>(p.llr);
   const std::int64_t total_warps = static_cast<std::int64_t>(gridDim.x) * kWarps;
 
-  for (std::int64_t m = p.frame_begin + gwarp; m < p.frame_end; m += total_warps) {
-    const FrameGeom g(m, p.n, p.f, p.v1, p.v2, p.f0);
+  for (std::int64_t mi = p.frame_begin + gwarp; mi < p.frame_end; mi += total_warps) {
+    const FrameRef fr = resolve_frame(p, mi);
+    const std::int64_t m = fr.m;  // block-local frame index (geometry, random-start salt)
+    const FrameGeom g(m, fr.n, p.f, p.v1, p.v2, p.f0);
     const std::int64_t len = g.len();
     M* sp = sig0;
     M* sc = sig1;
@@ -93,7 +95,7 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
     for (std::int64_t t = 0; t < len; ++t) {
       if ((t & (kStage - 1)) == 0) {
         const std::int64_t cnt = imin(kStage, len - t) * p.b;
-        const In* src = llr + (g.beg + t - p.llr_stage0) * p.b;
+        const In* src = llr + (fr.base + g.beg + t - p.llr_stage0) * p.b;
         __syncwarp();
         for (std::int64_t i = lane; i < cnt; i += 32) stage_buf[i] = src[i];
         __syncwarp();
@@ -172,9 +174,9 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
     if (p.sigma) {
       for (int j = lane; j < S; j += 32) {
         if constexpr (std::is_integral<M>::value) {
-          static_cast<std::int64_t*>(p.sigma)[(m - p.frame_begin) * S + j] = static_cast<std::int64_t>(sp[j]) + offset;
+          static_cast<std::int64_t*>(p.sigma)[(mi - p.frame_begin) * S + j] = static_cast<std::int64_t>(sp[j]) + offset;
         } else {
-          static_cast<double*>(p.sigma)[(m - p.frame_begin) * S + j] = sp[j];
+          static_cast<double*>(p.sigma)[(mi - p.frame_begin) * S + j] = sp[j];
         }
       }
     }
@@ -196,7 +198,7 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
       for (std::int64_t t = st; t >= lo - g.beg; --t) {
         const std::int64_t stage = g.beg + t;
         if (stage < hi) {
-          const std::int64_t rel = stage - p.out_stage0;
+          const std::int64_t rel = fr.base + stage - p.out_stage0;
           const std::int64_t w = rel >> 5;
           if (w != cur) {
             if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
@@ -273,8 +275,10 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
     return neg ? -acc : acc;
   };
 
-  for (std::int64_t m = p.frame_begin + gwarp; m < p.frame_end; m += total_warps) {
-    const FrameGeom g(m, p.n, p.f, p.v1, p.v2, p.f0);
+  for (std::int64_t mi = p.frame_begin + gwarp; mi < p.frame_end; mi += total_warps) {
+    const FrameRef fr = resolve_frame(p, mi);
+    const std::int64_t m = fr.m;  // block-local frame index (geometry, random-start salt)
+    const FrameGeom g(m, fr.n, p.f, p.v1, p.v2, p.f0);
     const std::int64_t len = g.len();
     M sig[NPL];
 #pragma unroll
@@ -282,7 +286,7 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
     std::int64_t offset = 0;
     std::int64_t next_record = 0;
     std::int64_t next_start = g.start_stage(0, p.v2);
-    const In* src = llr + (g.beg - p.llr_stage0) * b;
+    const In* src = llr + (fr.base + g.beg - p.llr_stage0) * b;
 
     auto refill = [&](std::int64_t t) {
       const std::int64_t cnt = imin(kStage, len - t) * b;
@@ -386,9 +390,9 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
         const int j = r * 32 + lane;
         if (!valid[r]) continue;
         if constexpr (std::is_integral<M>::value) {
-          static_cast<std::int64_t*>(p.sigma)[(m - p.frame_begin) * S + j] = static_cast<std::int64_t>(sig[r]) + offset;
+          static_cast<std::int64_t*>(p.sigma)[(mi - p.frame_begin) * S + j] = static_cast<std::int64_t>(sig[r]) + offset;
         } else {
-          static_cast<double*>(p.sigma)[(m - p.frame_begin) * S + j] = sig[r];
+          static_cast<double*>(p.sigma)[(mi - p.frame_begin) * S + j] = sig[r];
         }
       }
     }
@@ -414,7 +418,7 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
       auto step_one = [&](std::int64_t t, std::uint32_t word) {
         const std::int64_t stage = g.beg + t;
         if (stage < hi) {
-          const std::int64_t rel = stage - p.out_stage0;
+          const std::int64_t rel = fr.base + stage - p.out_stage0;
           const std::int64_t w = rel >> 5;
           if (w != cur) {
             if (cur >= 0 && acc) atomicOr(p.out + cur, acc);

@@ -23,7 +23,48 @@ struct DecodeLaunch {
   const std::uint32_t* in_out = nullptr;  // device copy of Trellis::in_out_ [S*2]
   std::uint32_t polys[8] = {};
   bool complement_paired = false;
+  // Batched mode (nblocks > 0): the stream is the concatenation of nblocks
+  // independent blocks (reference run_ber_sweep decodes every block with its
+  // own framed_decode call, berlab.cpp:63-88). Block j spans stages
+  // [blk_stage[j], blk_stage[j+1]) and global frames [blk_frame[j],
+  // blk_frame[j+1]); its frames are clipped at the block ends and their
+  // random-start salt uses the block-local frame index. Frame indices in
+  // [frame_begin, frame_end) are global; n is the total stage count.
+  int nblocks = 0;
+  const std::int64_t* blk_stage = nullptr;  // device [nblocks + 1]
+  const std::int64_t* blk_frame = nullptr;  // device [nblocks + 1]
+  const std::int32_t* blk_ilo = nullptr;    // device [nblocks]: fast-kernel frames are local [ilo, ihi)
+  const std::int32_t* blk_ihi = nullptr;
+  // Generic kernels only: process frame_list[frame_begin .. frame_end) (global
+  // frame ids) instead of the index range itself.
+  const std::int64_t* frame_list = nullptr;
+  std::int64_t safe_stage = 0;  // batched fast launch: window start of some interior frame
 };
+
+/// A global frame id resolved to its block: block-local frame index, block
+/// length and the block's first stage in the concatenated stream.
+struct FrameRef {
+  std::int64_t m, n, base;
+  int blk;
+};
+
+#ifdef __CUDACC__
+__device__ __forceinline__ FrameRef resolve_frame(const DecodeLaunch& p, std::int64_t idx) {
+  const std::int64_t g = p.frame_list ? __ldg(p.frame_list + idx) : idx;
+  if (p.nblocks == 0) return FrameRef{g, p.n, 0, 0};
+  int lo = 0, hi = p.nblocks;  // blk_frame[lo] <= g < blk_frame[hi]
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (__ldg(p.blk_frame + mid) <= g) {
+      lo = mid;
+    } else {
+      hi = mid;
+    }
+  }
+  const std::int64_t b0 = __ldg(p.blk_stage + lo);
+  return FrameRef{g - __ldg(p.blk_frame + lo), __ldg(p.blk_stage + lo + 1) - b0, b0, lo};
+}
+#endif
 
 /// Generic sm_100a kernel (any K in [2, 12], B in [2, 8]); int8 LLRs with
 /// int32 metrics or double LLRs with double metrics.

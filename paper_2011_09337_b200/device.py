@@ -40,6 +40,23 @@ def decode_f64_device(trellis: Trellis, cfg: FrameConfig, n: int, llr, llr_stage
                                      int(device), _stream(stream)))
 
 
+def decode_batch_i8_device(trellis: Trellis, cfg: FrameConfig, block_stages, llr, out, device: int = -1,
+                           stream=None):
+    """vd_decode_batch_i8_device: independent blocks (host list of stage
+    counts) concatenated in the int8 device tensor ``llr``; packed bits of
+    every block, back to back, into ``out``. Returns the summed stats."""
+    import numpy as np
+
+    from ._lib import VdStats
+
+    lens = np.ascontiguousarray(np.asarray(block_stages, np.int64))
+    c = cfg.to_c()
+    st = VdStats()
+    check(lib().vd_decode_batch_i8_device(trellis.handle, C.byref(c), int(lens.size), lens.ctypes.data, _ptr(llr),
+                                          _ptr(out), C.byref(st), int(device), _stream(stream)))
+    return st
+
+
 def synth_llr_i8(trellis: Trellis, n: int, sigma: float, scale: float, seed: int, llr, bits=None, device: int = -1,
                  stream=None) -> None:
     """Fill an int8 device tensor with n stages of synthetic AWGN LLRs."""
