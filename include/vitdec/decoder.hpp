@@ -77,4 +77,13 @@ struct ExecOptions {
 DecodeStats framed_decode(const std::int8_t* llr, std::int64_t n_stages, const Trellis& trellis,
                           const FrameConfig& cfg, std::uint32_t* packed_out, const ExecOptions& exec = {});
 
+/// framed_decode(depuncture(stream, pattern), trellis, cfg) — the chain the
+/// reference BER harness and CLI run (berlab.cpp:79-84, vitdec_cli.cpp:172-176)
+/// — on an int8 punctured stream: only the punctured bytes cross PCIe and the
+/// depuncture runs on the device. packed_out holds ceil(n_stages / 32) words,
+/// n_stages as reference depuncture derives it (decoder.cpp:141-152).
+DecodeStats framed_decode_punctured(const std::int8_t* punctured, std::int64_t n_punctured,
+                                    const PuncturePattern& pattern, const Trellis& trellis, const FrameConfig& cfg,
+                                    std::uint32_t* packed_out, const ExecOptions& exec = {});
+
 }  // namespace vitdec

@@ -169,6 +169,44 @@ vd_status vd_decode_i8(const vd_code* code, const vd_frame_cfg* cfg, const int8_
                        uint32_t* out_packed, vd_stats* stats, const vd_exec* exec);
 vd_status vd_decode_f64(const vd_code* code, const vd_frame_cfg* cfg, const double* llr, int64_t n_stages,
                         uint32_t* out_packed, vd_stats* stats, const vd_exec* exec);
+/* ---- puncturing (reference codec.hpp:13-33, decoder.hpp:69-72) ----------- */
+
+/* PuncturePattern: B rows x period columns, mask[col * b + row] in {0, 1}
+ * (1 keeps the bit), column-major as reference codec.hpp:15-21. */
+typedef struct {
+  int32_t b;
+  int32_t period;
+  const uint8_t* mask;
+} vd_puncture;
+
+/* PuncturePattern::validate (reference codec.cpp:12-23); VD_EUNSUPPORTED when
+ * period * b > 1024 (GPU depuncture table limit). */
+vd_status vd_puncture_validate(const vd_puncture* pattern);
+/* Stages covered by a punctured stream of n_punctured values; VD_EINVAL
+ * "punctured length inconsistent with pattern" exactly when reference
+ * depuncture throws (decoder.cpp:141-152). */
+vd_status vd_depuncture_stages(const vd_puncture* pattern, int64_t n_punctured, int64_t* n_stages);
+/* depuncture (reference decoder.cpp:131-163) on the device: llr_dev
+ * (4-byte aligned, n_stages * b bytes) receives the stage-major int8 block
+ * with 0 at every punctured position. Asynchronous. */
+vd_status vd_depuncture_i8_device(const vd_puncture* pattern, const int8_t* punctured_dev, int64_t n_punctured,
+                                  int8_t* llr_dev, int32_t device, void* stream);
+/* framed_decode(depuncture(stream, pattern), trellis, cfg) — the composition
+ * reference run_ber_sweep and the CLI run (berlab.cpp:79-84,
+ * vitdec_cli.cpp:172-176) — on host buffers: only the punctured bytes cross
+ * PCIe; each streamed chunk is depunctured on the device right before its
+ * decode. Output and stats as vd_decode_i8 on the depunctured block. */
+vd_status vd_decode_punctured_i8(const vd_code* code, const vd_frame_cfg* cfg, const vd_puncture* pattern,
+                                 const int8_t* punctured, int64_t n_punctured, uint32_t* out_packed, vd_stats* stats,
+                                 const vd_exec* exec);
+/* Device-resident form: llr_scratch_dev (4-byte aligned, n_stages * b bytes,
+ * see vd_depuncture_stages) receives the depunctured block, then every frame
+ * is decoded into out_dev (ceil(n_stages / 32) words). Asynchronous; stats
+ * (may be NULL) is computed on the host. */
+vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg* cfg, const vd_puncture* pattern,
+                                        const int8_t* punctured_dev, int64_t n_punctured, int8_t* llr_scratch_dev,
+                                        uint32_t* out_dev, vd_stats* stats, int32_t device, void* stream);
+
 /* serial_decode (reference decoder.cpp:101-129): one frame, no overlap. */
 vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n_stages, uint32_t* out_packed,
                                vd_stats* stats, int32_t device);

@@ -61,6 +61,8 @@ _ORACLE_SIGS = {
     "gen_bench_block": (I32, [I32, I32, P, I64, DBL, U64, P, P]),
     "gen_sweep_block": (I32, [I32, I32, P, I64, DBL, U64, P, P]),
     "quantize_i8": (None, [P, I64, DBL, P]),
+    "puncture_i8": (I32, [I32, I32, P, P, I64, P, P]),
+    "depuncture_i8": (I32, [I32, I32, P, P, I64, P, I64, P]),
 }
 
 _REF_SIGS = {
@@ -197,3 +199,40 @@ def framed_decode_range_i8(k, b, polys, llr, n, f, v1, v2, f0, start, seed, fram
     o.check(o.fn("framed_decode_range_i8")(k, b, _polys(polys), llr.ctypes.data, n, f, v1, v2, f0, start,
                                            seed & (2**64 - 1), frame_begin, frame_end, bits.ctypes.data))
     return bits
+
+
+def _mask_arr(mask_rows):
+    """Rows as strings ("110;101", reference PuncturePattern::parse) -> (b, period, column-major u8 mask)."""
+    rows = mask_rows.split(";")
+    b, period = len(rows), len(rows[0])
+    m = np.zeros(b * period, np.uint8)
+    for r, line in enumerate(rows):
+        for c, ch in enumerate(line):
+            m[c * b + r] = ch == "1"
+    return b, period, m
+
+
+def puncture_i8(mask_rows: str, llr: np.ndarray, n_stages: int) -> np.ndarray:
+    """Oracle puncture (reference codec.cpp:88-103) of an int8 stage-major stream."""
+    b, period, m = _mask_arr(mask_rows)
+    llr = np.ascontiguousarray(llr, dtype=np.int8)
+    out = np.zeros(max(llr.size, 1), np.int8)
+    n_out = C.c_int64()
+    o = oracle()
+    o.check(o.fn("puncture_i8")(b, period, m.ctypes.data, llr.ctypes.data, n_stages, out.ctypes.data,
+                                C.addressof(n_out)))
+    return out[: n_out.value].copy()
+
+
+def depuncture_i8(mask_rows: str, punctured: np.ndarray):
+    """Oracle depuncture (reference decoder.cpp:131-163) -> (stage-major int8 block, n_stages)."""
+    b, period, m = _mask_arr(mask_rows)
+    punctured = np.ascontiguousarray(punctured, dtype=np.int8)
+    o = oracle()
+    stages = C.c_int64()
+    o.check(o.fn("depuncture_i8")(b, period, m.ctypes.data, punctured.ctypes.data, punctured.size, None, 0,
+                                  C.addressof(stages)))
+    out = np.zeros(max(stages.value * b, 1), np.int8)
+    o.check(o.fn("depuncture_i8")(b, period, m.ctypes.data, punctured.ctypes.data, punctured.size, out.ctypes.data,
+                                  out.size, C.addressof(stages)))
+    return out[: stages.value * b].copy(), stages.value

@@ -458,3 +458,64 @@ void vdo_quantize_i8(const double* y, int64_t len, double scale, int8_t* q) {
     q[i] = (int8_t)v;
   }
 }
+
+/* ---- puncturing -----------------------------------------------------------
+ * mask: b x period, column-major (mask[col * b + row], reference
+ * codec.hpp:15-21). validate = PuncturePattern::validate (codec.cpp:12-23). */
+static int punct_validate(int b, int period, const uint8_t* mask) {
+  if (b < 1 || period < 1 || !mask) return fail("puncture mask shape mismatch");
+  for (int col = 0; col < period; ++col) {
+    int kept = 0;
+    for (int row = 0; row < b; ++row) kept += mask[col * b + row];
+    if (kept == 0) return fail("puncture mask drops an entire stage");
+  }
+  return 0;
+}
+
+/* puncture (codec.cpp:88-103), on int8 soft values instead of bits: keeps
+ * the mask-1 positions of a stage-major stream of n_stages stages. Writes
+ * *out_len values. */
+int vdo_puncture_i8(int b, int period, const uint8_t* mask, const int8_t* in, int64_t n_stages, int8_t* out,
+                    int64_t* out_len) {
+  if (punct_validate(b, period, mask)) return 1;
+  int64_t idx = 0;
+  for (int64_t t = 0; t < n_stages; ++t) {
+    const int col = (int)(t % period);
+    for (int row = 0; row < b; ++row) {
+      if (mask[col * b + row]) out[idx++] = in[t * b + row];
+    }
+  }
+  *out_len = idx;
+  return 0;
+}
+
+/* depuncture (decoder.cpp:131-163): stage count from the punctured length
+ * (throws "punctured length inconsistent with pattern"), then 0 at every
+ * punctured position. out (may be NULL: count only) holds out_cap values. */
+int vdo_depuncture_i8(int b, int period, const uint8_t* mask, const int8_t* in, int64_t len, int8_t* out,
+                      int64_t out_cap, int64_t* stages_out) {
+  if (punct_validate(b, period, mask)) return 1;
+  int per_period = 0;
+  for (int i = 0; i < b * period; ++i) per_period += mask[i];
+  int64_t remaining = len;
+  int64_t stages = (remaining / per_period) * period;
+  remaining %= per_period;
+  for (int col = 0; remaining > 0; ++col) {
+    int kept = 0;
+    if (col < period) {
+      for (int row = 0; row < b; ++row) kept += mask[col * b + row];
+    }
+    if (col >= period || remaining < kept) return fail("punctured length inconsistent with pattern");
+    remaining -= kept;
+    ++stages;
+  }
+  *stages_out = stages;
+  if (!out) return 0;
+  if (stages * b > out_cap) return fail("output buffer too small");
+  int64_t idx = 0;
+  for (int64_t t = 0; t < stages; ++t) {
+    const int col = (int)(t % period);
+    for (int row = 0; row < b; ++row) out[t * b + row] = mask[col * b + row] ? in[idx++] : 0;
+  }
+  return 0;
+}

@@ -11,13 +11,16 @@ from .api import (
     DecodeOutput,
     DecodeStats,
     FrameConfig,
+    PuncturePattern,
     TracebackStart,
     Trellis,
     build_trellis,
+    depuncture_stages,
     frame_stats,
     frame_window,
     framed_decode,
     framed_decode_batch,
+    framed_decode_punctured,
     framed_decode_stream,
     pack_bits,
     partition_frames,
@@ -33,13 +36,16 @@ __all__ = [
     "DecodeOutput",
     "DecodeStats",
     "FrameConfig",
+    "PuncturePattern",
     "TracebackStart",
     "Trellis",
     "build_trellis",
+    "depuncture_stages",
     "frame_stats",
     "frame_window",
     "framed_decode",
     "framed_decode_batch",
+    "framed_decode_punctured",
     "framed_decode_stream",
     "pack_bits",
     "partition_frames",

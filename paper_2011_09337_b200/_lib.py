@@ -38,6 +38,12 @@ class VdStats(C.Structure):
     _fields_ = [("frames", C.c_int64), ("stages", C.c_int64), ("tracebacks", C.c_int64)]
 
 
+class VdPuncture(C.Structure):
+    """struct vd_puncture (reference codec.hpp:13-33 PuncturePattern)."""
+
+    _fields_ = [("b", C.c_int32), ("period", C.c_int32), ("mask", C.c_void_p)]
+
+
 class VdExec(C.Structure):
     _fields_ = [("num_devices", C.c_int32), ("devices", C.POINTER(C.c_int32)), ("chunk_stages", C.c_int64)]
 
@@ -67,6 +73,13 @@ SIGNATURES = {
     "vd_serial_decode_f64": (I32, [P, P, I64, P, C.POINTER(VdStats), I32]),
     "vd_synth_llr_i8_device": (I32, [P, I64, DBL, DBL, U64, P, P, I32, P]),
     "vd_count_bit_errors_device": (I32, [P, P, I64, P, I32, P]),
+    "vd_puncture_validate": (I32, [C.POINTER(VdPuncture)]),
+    "vd_depuncture_stages": (I32, [C.POINTER(VdPuncture), I64, C.POINTER(I64)]),
+    "vd_depuncture_i8_device": (I32, [C.POINTER(VdPuncture), P, I64, P, I32, P]),
+    "vd_decode_punctured_i8": (I32, [P, C.POINTER(VdFrameCfg), C.POINTER(VdPuncture), P, I64, P, C.POINTER(VdStats),
+                                     C.POINTER(VdExec)]),
+    "vd_decode_punctured_i8_device": (I32, [P, C.POINTER(VdFrameCfg), C.POINTER(VdPuncture), P, I64, P, P,
+                                            C.POINTER(VdStats), I32, P]),
     "vd_last_error": (C.c_char_p, []),
     "vd_version": (C.c_char_p, []),
 }

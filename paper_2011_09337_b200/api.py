@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import VdExec, VdFrameCfg, VdStats, check, lib
+from ._lib import VdPuncture, VdExec, VdFrameCfg, VdStats, check, lib
 
 __all__ = [
     "CodeSpec",
@@ -335,3 +335,91 @@ def frame_window(cfg: FrameConfig, n: int, frame_begin: int, frame_end: int):
     b, e = C.c_int64(), C.c_int64()
     check(lib().vd_frame_window(C.byref(c), n, frame_begin, frame_end, C.byref(b), C.byref(e)))
     return int(b.value), int(e.value)
+
+
+# ---- puncturing (reference codec.hpp:13-33, decoder.hpp:69-72) -------------------
+
+
+class PuncturePattern:
+    """reference codec.hpp:13-33: B rows x ``period`` columns, column-major
+    ``mask[col * b + row]`` (1 keeps the coded bit)."""
+
+    def __init__(self, b: int, period: int, mask, name: str = ""):
+        self.b = int(b)
+        self.period = int(period)
+        self.mask = np.ascontiguousarray(np.asarray(mask, dtype=np.uint8).reshape(-1))
+        self.name = name
+
+    @staticmethod
+    def parse(rows: str) -> "PuncturePattern":
+        """reference codec.cpp:25-58: rows separated by ';', e.g. "110;101"."""
+        lines = rows.split(";")
+        b, period = len(lines), len(lines[0])
+        mask = np.zeros(b * period, np.uint8)
+        for r, line in enumerate(lines):
+            if len(line) != period:
+                raise ValueError("puncture mask rows differ in length")
+            for c, ch in enumerate(line):
+                if ch not in "01":
+                    raise ValueError("puncture mask must be 0/1")
+                mask[c * b + r] = ch == "1"
+        p = PuncturePattern(b, period, mask, rows)
+        p.validate()
+        return p
+
+    @staticmethod
+    def named(name: str) -> "PuncturePattern":
+        """reference codec.cpp:60-74: "r12", "r23", "r34" or an explicit mask."""
+        table = {"r12": "1;1", "r23": "11;10", "r34": "110;101"}
+        p = PuncturePattern.parse(table.get(name, name))
+        p.name = name
+        return p
+
+    def at(self, row: int, col: int) -> int:
+        return int(self.mask[col * self.b + row])
+
+    def kept_per_period(self) -> int:
+        return int(self.mask.sum())
+
+    def rate(self) -> float:
+        return self.period / self.kept_per_period()
+
+    def is_identity(self) -> bool:
+        return self.kept_per_period() == self.b * self.period
+
+    def to_c(self) -> VdPuncture:
+        return VdPuncture(self.b, self.period, self.mask.ctypes.data)
+
+    def validate(self) -> None:
+        """reference codec.cpp:12-23 (VD_EINVAL -> ValueError, same message)."""
+        c = self.to_c()
+        check(lib().vd_puncture_validate(C.byref(c)))
+
+
+def depuncture_stages(n_punctured: int, pattern: PuncturePattern) -> int:
+    """Stages a punctured stream covers (reference decoder.cpp:141-152 rules)."""
+    c = pattern.to_c()
+    n = C.c_int64()
+    check(lib().vd_depuncture_stages(C.byref(c), int(n_punctured), C.byref(n)))
+    return int(n.value)
+
+
+def framed_decode_punctured(punctured: np.ndarray, pattern: PuncturePattern, trellis: Trellis, cfg: FrameConfig,
+                            gpus: int = 0, chunk_stages: int = 0):
+    """framed_decode(depuncture(stream, pattern), trellis, cfg) (reference
+    berlab.cpp:79-84, vitdec_cli.cpp:172-176) on an int8 punctured stream:
+    only the punctured bytes go over PCIe, depuncture runs on the device
+    (vd_decode_punctured_i8). Returns (packed uint32 bits, n_stages, DecodeStats)."""
+    arr = np.ascontiguousarray(punctured)
+    if arr.dtype != np.int8:
+        raise TypeError("punctured stream must be int8")
+    arr = arr.reshape(-1)
+    n = depuncture_stages(arr.size, pattern)
+    out = np.zeros(max((n + 31) // 32, 1), np.uint32)
+    st = VdStats()
+    c = cfg.to_c()
+    pc = pattern.to_c()
+    ex = _exec(gpus, chunk_stages)
+    check(lib().vd_decode_punctured_i8(trellis.handle, C.byref(c), C.byref(pc), arr.ctypes.data, arr.size,
+                                       out.ctypes.data, C.byref(st), C.byref(ex)))
+    return out, n, _stats(st)

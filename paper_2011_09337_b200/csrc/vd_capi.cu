@@ -105,6 +105,87 @@ vd_status check_gpu_envelope(const vd_code* code) {
   return VD_OK;
 }
 
+// ---- puncturing (reference codec.hpp:13-33, codec.cpp:12-23, decoder.cpp:131-163)
+struct PunctPlan {
+  int b = 0, period = 0, kept = 0;  // kept = kept_per_period()
+  std::vector<std::int64_t> srank;  // kept bytes of columns [0, col): period + 1 entries
+  std::vector<std::int16_t> rank;   // per cell (col * b + row): kept index in the period, or -1
+  // absolute offset in the punctured stream of stage t's first kept byte
+  std::int64_t off(std::int64_t t) const { return (t / period) * kept + srank[t % period]; }
+};
+
+// PuncturePattern::validate (codec.cpp:12-23) plus the GPU envelope.
+vd_status make_punct(const vd_puncture* pat, PunctPlan* pp) {
+  if (!pat || !pat->mask || pat->b < 1 || pat->period < 1) return fail(VD_EINVAL, "puncture mask shape mismatch");
+  if (static_cast<std::int64_t>(pat->b) * pat->period > vd::kMaxPunctureCells) {
+    return fail(VD_EUNSUPPORTED, "GPU depuncture supports period * B <= 1024");
+  }
+  pp->b = pat->b;
+  pp->period = pat->period;
+  pp->kept = 0;
+  pp->srank.assign(static_cast<std::size_t>(pat->period) + 1, 0);
+  pp->rank.assign(static_cast<std::size_t>(pat->period) * pat->b, -1);
+  for (int col = 0; col < pat->period; ++col) {
+    int kept = 0;
+    for (int row = 0; row < pat->b; ++row) {
+      const std::uint8_t m = pat->mask[col * pat->b + row];
+      if (m > 1) return fail(VD_EINVAL, "puncture mask must be 0/1");
+      if (m) pp->rank[col * pat->b + row] = static_cast<std::int16_t>(pp->kept + kept++);
+    }
+    if (kept == 0) return fail(VD_EINVAL, "puncture mask drops an entire stage");
+    pp->kept += kept;
+    pp->srank[col + 1] = pp->kept;
+  }
+  return VD_OK;
+}
+
+// Stage count of a punctured stream (decoder.cpp:141-152).
+vd_status punct_stages(const PunctPlan& pp, std::int64_t len, std::int64_t* stages) {
+  if (len < 0) return fail(VD_EINVAL, "punctured length inconsistent with pattern");
+  std::int64_t st = (len / pp.kept) * pp.period;
+  std::int64_t rem = len % pp.kept;
+  for (int col = 0; rem > 0; ++col) {
+    const std::int64_t ck = pp.srank[col + 1] - pp.srank[col];
+    if (col >= pp.period || rem < ck) return fail(VD_EINVAL, "punctured length inconsistent with pattern");
+    rem -= ck;
+    ++st;
+  }
+  *stages = st;
+  return VD_OK;
+}
+
+// Depuncture stages [t0, t0 + n) from `in` (= the punctured stream at offset off(t0)).
+vd_status launch_depuncture(const PunctPlan& pp, const std::int8_t* in, std::int64_t t0, std::int64_t n,
+                            std::int8_t* out, cudaStream_t s) {
+  vd::DepunctureLaunch d;
+  d.in = in;
+  d.in0 = pp.off(t0);
+  d.out = out;
+  d.t0 = t0;
+  d.n = n;
+  d.b = pp.b;
+  d.period = pp.period;
+  d.kept = pp.kept;
+  d.in_len = pp.off(t0 + n) - d.in0;
+  // unit = U whole periods, >= 1 KiB of output; U * period * b a multiple of
+  // 16 and U * kept a multiple of 4 (unit-invariant byte alignment); tile =
+  // tu units, ~32 KiB of output per shared-memory staging round
+  const int pb = pp.period * pp.b;
+  int unit = 16;
+  for (int x = pb; x % 2 == 0 && unit > 1; x /= 2) unit /= 2;  // 16 / gcd(pb, 16)
+  int unit_in = 4;
+  for (int x = pp.kept; x % 2 == 0 && unit_in > 1; x /= 2) unit_in /= 2;  // 4 / gcd(kept, 4)
+  unit = std::max(unit, unit_in);                                          // both powers of two
+  d.unit_periods = std::max(unit, (1024 / pb + unit - 1) / unit * unit);
+  d.unit_bytes = d.unit_periods * pb;
+  d.unit_in = d.unit_periods * pp.kept;
+  d.tu = std::max(1, 32768 / d.unit_bytes);
+  std::copy(pp.rank.begin(), pp.rank.end(), d.rank);
+  const cudaError_t e = vd::launch_depuncture_i8(d, s);
+  if (e != cudaSuccess) return cuda_fail(e, "depuncture kernel");
+  return VD_OK;
+}
+
 vd_status device_table(const vd_code* code, int device, const std::uint32_t** out) {
   std::lock_guard<std::mutex> lk(code->mu);
   auto it = code->dev_in_out.find(device);
@@ -378,6 +459,8 @@ struct DevCtx {
   std::size_t llr_cap[2] = {0, 0};
   std::uint32_t* out[2] = {nullptr, nullptr};
   std::size_t out_cap[2] = {0, 0};
+  void* pun[2] = {nullptr, nullptr};  // punctured-stream staging (depuncture input)
+  std::size_t pun_cap[2] = {0, 0};
 };
 
 struct ThreadCtx {
@@ -388,6 +471,7 @@ struct ThreadCtx {
       for (int i = 0; i < 2; ++i) {
         if (kv.second.llr[i]) cudaFree(kv.second.llr[i]);
         if (kv.second.out[i]) cudaFree(kv.second.out[i]);
+        if (kv.second.pun[i]) cudaFree(kv.second.pun[i]);
         if (kv.second.st[i]) cudaStreamDestroy(kv.second.st[i]);
       }
     }
@@ -410,9 +494,13 @@ struct Chunk {
   std::int64_t f0, f1;  // frame range
 };
 
+// pp != nullptr (int8 only): `llr` is the PUNCTURED stream of pattern pp
+// covering n stages; each chunk's punctured bytes are copied and expanded on
+// the device (depuncture kernel) right before its decode.
 template <typename T>
 vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr, std::int64_t n,
-                      std::uint32_t* out_packed, vd_stats* stats, const vd_exec* exec) {
+                      std::uint32_t* out_packed, vd_stats* stats, const vd_exec* exec,
+                      const PunctPlan* pp = nullptr) {
   if (!code) return fail(VD_EINVAL, "null code");
   if (n < 1) return fail(VD_EINVAL, "empty llr block");
   if (vd_status st = validate_cfg(cfg, 1)) return st;
@@ -471,6 +559,9 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
     for (int i = 0; i < 2; ++i) {
       if (!ctx.st[i]) VD_CUDA(cudaStreamCreateWithFlags(&ctx.st[i], cudaStreamNonBlocking), "cudaStreamCreate");
       if (vd_status st = ensure(&ctx.llr[i], &ctx.llr_cap[i], llr_bytes)) return st;
+      if (pp) {
+        if (vd_status st = ensure(&ctx.pun[i], &ctx.pun_cap[i], llr_bytes)) return st;
+      }
       void* o = ctx.out[i];
       if (vd_status st = ensure(&o, &ctx.out_cap[i], out_bytes)) return st;
       ctx.out[i] = static_cast<std::uint32_t*>(o);
@@ -490,8 +581,17 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
       std::int64_t wb = 0, we = 0;
       if (vd_status st = vd_frame_window(cfg, n, c.f0, c.f1, &wb, &we)) return st;
       T* dl = static_cast<T*>(ctx.llr[slot]);
-      VD_CUDA(cudaMemcpyAsync(dl, llr + wb * code->b, sizeof(T) * (we - wb) * code->b, cudaMemcpyHostToDevice, s),
-              "H2D llr chunk");
+      if (pp) {
+        const std::int64_t p0 = pp->off(wb), p1 = pp->off(we);
+        VD_CUDA(cudaMemcpyAsync(ctx.pun[slot], llr + p0, sizeof(T) * (p1 - p0), cudaMemcpyHostToDevice, s),
+                "H2D punctured chunk");
+        if (vd_status st = launch_depuncture(*pp, static_cast<const std::int8_t*>(ctx.pun[slot]), wb, we - wb,
+                                             reinterpret_cast<std::int8_t*>(dl), s))
+          return st;
+      } else {
+        VD_CUDA(cudaMemcpyAsync(dl, llr + wb * code->b, sizeof(T) * (we - wb) * code->b, cudaMemcpyHostToDevice, s),
+                "H2D llr chunk");
+      }
       const std::int64_t out_lo = c.f0 * cfg->f;  // multiple of 32 by construction
       const std::int64_t out_hi = std::min<std::int64_t>(c.f1 * cfg->f, n);
       vd_status st = decode_device<T>(code, cfg, n, dl, wb, c.f0, c.f1, ctx.out[slot], out_lo, nullptr, devices[d], s);
@@ -725,6 +825,74 @@ vd_status vd_decode_i8(const vd_code* code, const vd_frame_cfg* cfg, const int8_
 vd_status vd_decode_f64(const vd_code* code, const vd_frame_cfg* cfg, const double* llr, int64_t n, uint32_t* out,
                         vd_stats* stats, const vd_exec* exec) {
   return decode_host<double>(code, cfg, llr, n, out, stats, exec);
+}
+
+vd_status vd_puncture_validate(const vd_puncture* pattern) {
+  PunctPlan pp;
+  return make_punct(pattern, &pp);
+}
+
+vd_status vd_depuncture_stages(const vd_puncture* pattern, int64_t n_punctured, int64_t* n_stages) {
+  PunctPlan pp;
+  if (vd_status st = make_punct(pattern, &pp)) return st;
+  if (!n_stages) return fail(VD_EINVAL, "null buffer");
+  return punct_stages(pp, n_punctured, n_stages);
+}
+
+vd_status vd_depuncture_i8_device(const vd_puncture* pattern, const int8_t* punctured_dev, int64_t n_punctured,
+                                  int8_t* llr_dev, int32_t device, void* stream) {
+  PunctPlan pp;
+  if (vd_status st = make_punct(pattern, &pp)) return st;
+  std::int64_t n = 0;
+  if (vd_status st = punct_stages(pp, n_punctured, &n)) return st;
+  if (n == 0) return VD_OK;
+  if (!punctured_dev || !llr_dev) return fail(VD_EINVAL, "null buffer");
+  if (reinterpret_cast<std::uintptr_t>(llr_dev) & 3u) return fail(VD_EINVAL, "llr_dev must be 4-byte aligned");
+  int dev = 0;
+  if (vd_status st = resolve_device(device, &dev)) return st;
+  DeviceGuard guard(dev);
+  return launch_depuncture(pp, punctured_dev, 0, n, llr_dev, static_cast<cudaStream_t>(stream));
+}
+
+// framed_decode(depuncture(stream, pattern), trellis, cfg): the composition
+// the reference's BER harness and CLI run (berlab.cpp:79-84, vitdec_cli.cpp:172-176).
+static vd_status punct_decode_prep(const vd_code* code, const vd_frame_cfg* cfg, const vd_puncture* pattern,
+                                   int64_t n_punctured, PunctPlan* pp, std::int64_t* n) {
+  if (!code) return fail(VD_EINVAL, "null code");
+  if (vd_status st = make_punct(pattern, pp)) return st;
+  if (vd_status st = punct_stages(*pp, n_punctured, n)) return st;
+  if (*n < 1) return fail(VD_EINVAL, "empty llr block");
+  if (pp->b != code->b) return fail(VD_EINVAL, "llr row count must equal B");  // check_block, decoder.cpp:92-97
+  return validate_cfg(cfg, 1);
+}
+
+vd_status vd_decode_punctured_i8(const vd_code* code, const vd_frame_cfg* cfg, const vd_puncture* pattern,
+                                 const int8_t* punctured, int64_t n_punctured, uint32_t* out_packed, vd_stats* stats,
+                                 const vd_exec* exec) {
+  PunctPlan pp;
+  std::int64_t n = 0;
+  if (vd_status st = punct_decode_prep(code, cfg, pattern, n_punctured, &pp, &n)) return st;
+  return decode_host<std::int8_t>(code, cfg, punctured, n, out_packed, stats, exec, &pp);
+}
+
+vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg* cfg, const vd_puncture* pattern,
+                                        const int8_t* punctured_dev, int64_t n_punctured, int8_t* llr_scratch_dev,
+                                        uint32_t* out_dev, vd_stats* stats, int32_t device, void* stream) {
+  PunctPlan pp;
+  std::int64_t n = 0;
+  if (vd_status st = punct_decode_prep(code, cfg, pattern, n_punctured, &pp, &n)) return st;
+  if (stats) {
+    if (vd_status st = vd_frame_stats(cfg, n, stats)) return st;
+  }
+  if (!punctured_dev || !llr_scratch_dev || !out_dev) return fail(VD_EINVAL, "null buffer");
+  if (reinterpret_cast<std::uintptr_t>(llr_scratch_dev) & 3u) return fail(VD_EINVAL, "llr_scratch_dev must be 4-byte aligned");
+  int dev = 0;
+  if (vd_status st = resolve_device(device, &dev)) return st;
+  DeviceGuard guard(dev);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (vd_status st = launch_depuncture(pp, punctured_dev, 0, n, llr_scratch_dev, s)) return st;
+  return decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, 0, 0, num_frames(cfg, n), out_dev, 0, nullptr,
+                                    dev, stream);
 }
 
 vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n, uint32_t* out, vd_stats* stats,

@@ -76,6 +76,27 @@ cudaError_t launch_generic_f64(const DecodeLaunch& p, cudaStream_t stream);
 bool fast_path_supported(const DecodeLaunch& p);
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream);
 
+/// Device depuncture of stages [t0, t0 + n) (reference decoder.cpp:131-163):
+/// out[(t - t0) * b + row] = mask(row, t % period) ? next punctured byte : 0.
+/// `in` points at the first kept byte of stage t0, whose absolute offset in
+/// the punctured stream is in0. rank[q] (q = col * b + row, the reference's
+/// column-major mask order) is the kept index of position q inside its period,
+/// or -1 when q is punctured. `in` holds in_len bytes. A unit is
+/// unit_periods whole periods: unit_bytes = unit_periods * period * b output
+/// bytes (a multiple of 16), unit_in = unit_periods * kept input bytes (a
+/// multiple of 4); a tile (one shared-memory staging round) is tu units.
+constexpr int kMaxPunctureCells = 1024;  // period * b
+struct DepunctureLaunch {
+  const std::int8_t* in = nullptr;
+  std::int64_t in0 = 0, in_len = 0;
+  std::int8_t* out = nullptr;  // 4-byte aligned
+  std::int64_t t0 = 0, n = 0;
+  int b = 0, period = 0, kept = 0;
+  int unit_periods = 0, unit_bytes = 0, unit_in = 0, tu = 0;
+  std::int16_t rank[kMaxPunctureCells] = {};
+};
+cudaError_t launch_depuncture_i8(const DepunctureLaunch& p, cudaStream_t stream);
+
 cudaError_t launch_synth_i8(int k, int b, const std::uint32_t* polys, std::int64_t n, double sigma, double scale,
                             std::uint64_t seed, std::int8_t* llr, std::uint32_t* bits, cudaStream_t stream);
 cudaError_t launch_count_bit_errors(const std::uint32_t* a, const std::uint32_t* b, std::int64_t n_bits,

@@ -267,4 +267,21 @@ DecodeStats framed_decode(const std::int8_t* llr, std::int64_t n_stages, const T
   return from_c(st);
 }
 
+DecodeStats framed_decode_punctured(const std::int8_t* punctured, std::int64_t n_punctured,
+                                    const PuncturePattern& pattern, const Trellis& trellis, const FrameConfig& cfg,
+                                    std::uint32_t* packed_out, const ExecOptions& exec) {
+  cfg.validate();
+  const vd_frame_cfg c = to_c(cfg);
+  const vd_puncture pc{pattern.b, pattern.period, pattern.mask.data()};
+  if (static_cast<int>(pattern.mask.size()) != pattern.b * pattern.period) {
+    throw std::invalid_argument("puncture mask shape mismatch");
+  }
+  vd_stats st{};
+  vd_exec ex{};
+  ex.num_devices = exec.gpus > 0 ? exec.gpus : 1;
+  ex.chunk_stages = exec.chunk_stages;
+  check(vd_decode_punctured_i8(trellis.native(), &c, &pc, punctured, n_punctured, packed_out, &st, &ex));
+  return from_c(st);
+}
+
 }  // namespace vitdec

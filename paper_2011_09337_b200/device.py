@@ -68,3 +68,22 @@ def synth_llr_i8(trellis: Trellis, n: int, sigma: float, scale: float, seed: int
 def count_bit_errors(a, b, n_bits: int, count, device: int = -1, stream=None) -> None:
     check(lib().vd_count_bit_errors_device(_ptr(a), _ptr(b), int(n_bits), _ptr(count), int(device),
                                            _stream(stream)))
+
+
+def depuncture_i8_device(pattern, punctured, n_punctured: int, llr, device: int = -1, stream=None) -> None:
+    """vd_depuncture_i8_device: punctured int8 device tensor -> stage-major
+    int8 block (0 at punctured positions) in ``llr`` (4-byte aligned)."""
+    pc = pattern.to_c()
+    check(lib().vd_depuncture_i8_device(C.byref(pc), _ptr(punctured), int(n_punctured), _ptr(llr), int(device),
+                                        _stream(stream)))
+
+
+def decode_punctured_i8_device(trellis: Trellis, cfg: FrameConfig, pattern, punctured, n_punctured: int, scratch,
+                               out, device: int = -1, stream=None) -> None:
+    """vd_decode_punctured_i8_device: device depuncture into ``scratch`` then
+    the framed decode of every frame into ``out``."""
+    c = cfg.to_c()
+    pc = pattern.to_c()
+    check(lib().vd_decode_punctured_i8_device(trellis.handle, C.byref(c), C.byref(pc), _ptr(punctured),
+                                              int(n_punctured), _ptr(scratch), _ptr(out), None, int(device),
+                                              _stream(stream)))
