@@ -231,6 +231,10 @@ struct FastParams {
   int t_first, t_split, s_base, smem_rows, tcols;
   int tm_alloc;  // TMEM columns allocated per CTA (power of two)
   std::int64_t safe_stage;  // window start of an interior frame (loads of empty frame slots)
+  // IMAD multipliers 1, 2, -1 read from the parameter bank: ptxas cannot
+  // constant-fold them, so the table / decision arithmetic written as
+  // mad_u32 stays on the FMA pipe instead of becoming ALU-pipe LEA / IADD3.
+  std::uint32_t one, two, m1;
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -261,6 +265,18 @@ __device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t 
 // Butterflies per stage whose decision words use the FMA-pipe form (balances
 // the ALU and FMA pipes; the rest use the one-instruction ALU form).
 constexpr int kFmaPairs = VD_FMA_PAIRS;
+#ifndef VD_PARAM_MULS
+#define VD_PARAM_MULS 0  // measured: 1 is 5 % slower (profiles/r01_ab_notes.md)
+#endif
+#ifndef VD_FMA_NEG
+#define VD_FMA_NEG 0
+#endif
+#ifndef VD_MERGED_STORE
+#define VD_MERGED_STORE 0  // measured 0.6 % slower than separate TMEM / smem block copies
+#endif
+#ifndef VD_LOCKSTEP
+#define VD_LOCKSTEP 1
+#endif
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2
 #endif
@@ -345,7 +361,10 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
       PT[k][3] = d - x2 + 0x01000100u;
     }
 #pragma unroll
-    for (int x = 0; x < GEO::NT; ++x) PT[k][x ^ XM] = OFFB - PT[k][x];  // T[x ^ XM] = -T[x]
+    for (int x = 0; x < GEO::NT; ++x) {
+      // T[x ^ XM] = -T[x]
+      PT[k][x ^ XM] = VD_FMA_NEG ? mad_u32(PT[k][x], st.m1, OFFB) : OFFB - PT[k][x];
+    }
   }
 }
 
@@ -388,8 +407,9 @@ __device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32
 
 // One block of LB stages. MODE 0 (slow) range-checks every pending store and
 // calls the stored-max argmax hook; MODE 1 / 2 are straight-line blocks whose
-// pending stores all go to shared memory / tensor memory; MODE 3 blocks lie
-// entirely in the v1 warm-up (ACS only: no decision words, no stores).
+// pending stores all go to shared memory / tensor memory, MODE 4 the same with
+// the target picked at run time (one code copy); MODE 3 blocks lie entirely
+// in the v1 warm-up (ACS only: no decision words, no stores).
 template <class C, class GEO, int MODE, bool TM, int BUF, class RecFn>
 __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
                                           const std::uint32_t* pfA, const std::uint32_t* pfB, int pf_room,
@@ -479,6 +499,18 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     }
   }
   if constexpr (MODE == 2) tmem_st4(bc.taddr + static_cast<std::uint32_t>(blk * LB - 1 - bc.t_first), tw);
+  if constexpr (MODE == 4) {
+    // merged straight-line block: the block's 4 words go to tensor memory or
+    // to shared memory (one warp-uniform branch; one code copy for both halves
+    // of the survivor store keeps the hot loop small in the instruction cache)
+    const int tp = blk * LB - 1;
+    if (TM && tp < bc.t_split) {
+      tmem_st4(bc.taddr + static_cast<std::uint32_t>(tp - bc.t_first), tw);
+    } else {
+#pragma unroll
+      for (int k = 0; k < LB; ++k) bc.drow_lane[(tp + k - bc.s_base) * 32] = tw[k];
+    }
+  }
   if constexpr (MODE != 0) tprev = blk * LB + LB - 1;
 }
 
@@ -519,7 +551,20 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     tbase = *tmem_slot;
   }
 
-  const std::int64_t gwarp = static_cast<std::int64_t>(blockIdx.x) * fp.warps_per_cta + warp;
+  // Persistent warps: the grid holds at most one CTA per SM and every warp
+  // walks frame groups gwarp, gwarp + W, ... (W = warps in the grid), so the
+  // TMEM allocation and CTA start-up are paid once per SM, and warps drift out
+  // of phase (one warp's traceback overlaps other warps' forward passes).
+  // All warps of a CTA run the same number of rounds and meet at a CTA
+  // barrier after each one: keeping the warps in phase measured faster than
+  // letting them drift (the forward and traceback code then compete for the
+  // instruction cache).
+  const std::int64_t wtotal = static_cast<std::int64_t>(gridDim.x) * fp.warps_per_cta;
+  const std::int64_t groups = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
+  const std::int64_t rounds = (groups + wtotal - 1) / wtotal;
+  for (std::int64_t rnd = 0; rnd < rounds; ++rnd) {
+  if (VD_LOCKSTEP && rnd > 0) __syncthreads();
+  const std::int64_t gwarp = rnd * wtotal + static_cast<std::int64_t>(blockIdx.x) * fp.warps_per_cta + warp;
   const std::int64_t mbase = fp.mi0 + gwarp * GEO::FPW;
   if (mbase < fp.mi1) {  // (no early return: TMEM dealloc needs every warp at the barrier)
   const std::int64_t mA = mbase + 2 * grp, mB = mA + 1;
@@ -582,9 +627,15 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
 #pragma unroll
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
   }
+#if VD_PARAM_MULS
+  st.one = fp.one;
+  st.two = fp.two;
+  st.m1 = fp.m1;
+#else
   st.one = opaque(1u);
   st.two = opaque(2u);
   st.m1 = opaque(0xffffffffu);
+#endif
 #pragma unroll
   for (int i = 0; i < R; ++i) st.sig[i] = BASE;
 #pragma unroll
@@ -747,6 +798,8 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     if (t0 + LB <= v1) {
       // warm-up block: every stage (and the next block's pending one) < v1
       run_block<C, GEO, 3, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+    } else if (VD_MERGED_STORE && clean && (t0 - 1 >= t_split || (TM && t0 + LB - 2 < t_split))) {
+      run_block<C, GEO, 4, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     } else if (clean && t0 - 1 >= t_split) {
       run_block<C, GEO, 1, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     } else if (TM && clean && t0 + LB - 2 < t_split) {
@@ -888,7 +941,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
       if (o + nb > 32) atomicOr(p.out + w0 + 1, word >> (32 - o));
     }
   }
+  __syncwarp();  // this group's traceback reads are done before the next group's stores
   }  // mbase < mi1
+  }  // rounds
 
   if constexpr (TM) {
     asm volatile("tcgen05.fence::before_thread_sync;");
@@ -966,6 +1021,9 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   using GEO = Geo<C, R>;
   FastParams fp{};
   fp.p = p;
+  fp.one = 1u;
+  fp.two = 2u;
+  fp.m1 = 0xffffffffu;
   fp.L = p.f + p.v1 + p.v2;
   fp.nblk = (fp.L + GEO::LB - 1) / GEO::LB;
   fp.step = p.f0 > 0 ? p.f0 : p.f;
@@ -1080,10 +1138,18 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
     if (cudaError_t err = cudaEventRecord(side->join, side->s); err != cudaSuccess) return err;
   }
   const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
-  const std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
+  std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
   auto kern = pl.tm ? fast_kernel<C, R, true> : fast_kernel<C, R, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem));
   if (e != cudaSuccess) return e;
+  // persistent grid: as many CTAs as are co-resident (one per SM with TMEM)
+  int per_sm = 1;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fp.warps_per_cta * 32, pl.smem) != cudaSuccess ||
+      per_sm < 1) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  blocks = std::min<std::int64_t>(blocks, static_cast<std::int64_t>(sm_count()) * per_sm);
   kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fp);
   e = cudaGetLastError();
   if (e == cudaSuccess && edges) e = cudaStreamWaitEvent(stream, side->join, 0);

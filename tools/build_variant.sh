@@ -10,8 +10,9 @@ mkdir -p "$out"
 SRC=$ROOT/paper_2011_09337_b200/csrc
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 -Xcompiler -fPIC --expt-relaxed-constexpr -I$ROOT/include -I$ROOT/third_party/eigen_shim -I$SRC $*"
 pids=()
-for f in vd_capi vd_fast vd_generic vd_synth; do
-  src=$SRC/$f.cu; [ "$f" = vd_fast ] && [ -n "$FAST_SRC" ] && src=$FAST_SRC
+for src0 in $SRC/*.cu; do
+  f=$(basename $src0 .cu)
+  src=$src0; [ "$f" = vd_fast ] && [ -n "$FAST_SRC" ] && src=$FAST_SRC
   nvcc $FL -c $src -o $out/$f.o & pids+=($!)
 done
 g++ -O2 -fPIC -std=c++17 -I$ROOT/include -I$ROOT/third_party/eigen_shim -I$SRC -I/usr/local/cuda/include -c $SRC/vitdec_api.cpp -o $out/vitdec_api.o
