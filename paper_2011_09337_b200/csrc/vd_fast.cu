@@ -277,6 +277,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_LOCKSTEP
 #define VD_LOCKSTEP 1
 #endif
+#ifndef VD_FAST_TB
+#define VD_FAST_TB 1
+#endif
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2
 #endif
@@ -856,6 +859,52 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     const std::uint32_t hsh = half ? 16u : 0u;
     const int gcol = (fr >> 1) * G;  // this frame's group: first lane of its decision columns
     const std::int64_t obase = sl.ws - p.out_stage0;  // output bit index of frame-relative stage 0
+    // ---- serial-traceback fast path: one task per frame, whole blocks from
+    // stage L-1 down to v1, output words aligned (f % 32 == 0). Per block:
+    // one 4-word fetch, 4 x (funnel shift + bit select), 4 emitted bits into
+    // a 32-bit accumulator stored with a plain 32-bit write every 8 blocks.
+    if (VD_FAST_TB && num_sub == 1 && (L & (LB - 1)) == 0 && (v1 & (LB - 1)) == 0 && (f & 31) == 0 &&
+        __all_sync(kFull, ((obase + v1) & 31) == 0)) {
+      std::uint32_t lp = P >> r;
+      std::uint32_t u = (P & (R - 1)) | hsh;  // bit index into a decision word: register + 16 * half
+      std::uint32_t acc32 = 0;
+      std::uint32_t* const outw = p.out + ((obase + v1) >> 5);
+      const int t_emit = v1 + f;  // blocks below this stage emit their 4 bits
+      auto step_block = [&](int tb0, const std::uint32_t (&wd)[LB]) {
+        const std::uint32_t rin = u & (R - 1);  // bit j = decoded bit of stage tb0 + j
+#pragma unroll
+        for (int j = LB - 1; j >= 0; --j) {
+          const std::uint32_t x = __funnelshift_r(wd[j], wd[j], u - static_cast<std::uint32_t>(j));  // bit u -> bit j
+          u = (x & (1u << j)) | (u & ~(1u << j));
+        }
+        if (tb0 < t_emit) {
+          acc32 = (acc32 << LB) | rin;
+          if (((tb0 - v1) & 31) == 0 && valid) outw[(tb0 - v1) >> 5] = acc32;
+        }
+        const std::uint32_t pa = (lp << r) | (u & (R - 1));
+        const std::uint32_t pn = ((pa << r) | (pa >> (M - r))) & GEO::SMASK;  // undo the block relayout
+        lp = pn >> r;
+        u = (pn & (R - 1)) | hsh;
+      };
+      int tb0 = L - LB;
+      for (; tb0 >= v1 && (!TM || tb0 >= t_split); tb0 -= LB) {  // shared-memory rows
+        std::uint32_t wd[LB];
+        const std::uint32_t* src = dec + (tb0 - s_base) * 32 + gcol + lp;
+#pragma unroll
+        for (int j = 0; j < LB; ++j) wd[j] = src[j * 32];
+        step_block(tb0, wd);
+      }
+      if constexpr (TM) {
+        for (; tb0 >= v1; tb0 -= LB) {  // tensor-memory columns
+          std::uint32_t own[4], wd[LB];
+          tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
+          step_block(tb0, wd);
+        }
+      }
+      continue;
+    }
     std::uint64_t acc = 0;  // emitted bits, newest (lowest stage) at bit 0
     int nb = 0;
     // Round-uniform bounds (inactive lanes have st_t = -1 and sub_lo = v1).
