@@ -37,6 +37,7 @@ sys.path.insert(0, str(ROOT))
 
 K7 = (7, 2, [0o171, 0o133])
 F, V1, V2 = 256, 20, 20
+F0 = 0
 SCALE = 32.0
 EBN0 = 3.0
 
@@ -62,7 +63,13 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--frame", default="", help="f,v1,v2[,f0] frame configuration override (default 256,20,20)")
     a = ap.parse_args()
+    if a.frame:
+        global F, V1, V2, F0
+        vals = [int(x) for x in a.frame.split(",")]
+        F, V1, V2 = vals[:3]
+        F0 = vals[3] if len(vals) > 3 else 0
     a.code, default_n, a.workload_desc = WORKLOADS[a.workload]
     if a.stages <= 0:
         a.stages = default_n
@@ -155,15 +162,15 @@ def cpu_reference_rate(target_s: float, threads: int | None = None, code=K7):
     rx, _ = port.gen_bench_block(*code, n, EBN0, 1)
     q = oracle.quantize(rx, SCALE)
     t0 = time.perf_counter()
-    backend.framed_decode(*code, q, n, F, V1, V2, workers=cores)
+    backend.framed_decode(*code, q, n, F, V1, V2, F0, workers=cores)
     rate = n / max(time.perf_counter() - t0, 1e-6)
     n = int(min(max(rate * target_s, 1 << 16), 1 << 26))
     rx, _ = port.gen_bench_block(*code, n, EBN0, 2)
     q = oracle.quantize(rx, SCALE)
     t0 = time.perf_counter()
-    backend.framed_decode(*code, q, n, F, V1, V2, workers=cores)
+    backend.framed_decode(*code, q, n, F, V1, V2, F0, workers=cores)
     dt = time.perf_counter() - t0
-    sample = (f"{n} info bits (K={code[0]} B={code[1]}, int8 q=rint(32y) at {EBN0} dB, f={F}/v1={V1}/v2={V2}), "
+    sample = (f"{n} info bits (K={code[0]} B={code[1]}, int8 q=rint(32y) at {EBN0} dB, f={F}/v1={V1}/v2={V2}/f0={F0}), "
               f"{'reference framed_decode, workers=' + str(cores) if ref else 'C oracle port, 1 thread'}")
     return n / dt / 1e9, cores, kind, sample, dt
 
@@ -221,7 +228,7 @@ def run_ours(args):
 
     t = vd.build_trellis(vd.CodeSpec(*args.code))
     B = args.code[1]
-    cfg = vd.FrameConfig(F, V1, V2)
+    cfg = vd.FrameConfig(F, V1, V2, F0)
     n = args.stages
     nf = (n + F - 1) // F
     stats = vd.frame_stats(cfg, n)
@@ -343,7 +350,8 @@ def run_ours(args):
             "dtype": "int8 LLR / int32 path metrics" if not t.fast_path() else "int8 LLR / int16x2 path metrics",
             "data": "synthetic: random message, K=7 encoder, BPSK+AWGN at 3 dB, int8 q=rint(32y), generated in HBM",
             "config": {
-                "workload": args.workload_desc,
+                "workload": args.workload_desc if not args.frame else
+                            f"{args.workload_desc.split(',')[0]}, frame override f={F} v1={V1} v2={V2} f0={F0}",
                 "info_bits_per_gpu_per_step": n,
                 "frames_per_gpu": nf,
                 "parallelism": f"frame shards x{world} (no collective)",

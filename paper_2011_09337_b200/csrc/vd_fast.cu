@@ -32,7 +32,9 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <map>
+#include <mutex>
 #include <type_traits>
 
 #include "vd_common.cuh"
@@ -229,6 +231,11 @@ struct FastParams {
   // lanes = the warp's lanes), stages [s_base, L) in shared memory rows
   // (row = t - s_base); row smem_rows - 1 is a dummy sink.
   int t_first, t_split, s_base, smem_rows, tcols;
+  // Long frames: stages [t_gl, L) spill to a global scratch (L2 / HBM),
+  // g_rows rows of 32 words per warp slot (slot = CTA * warps_per_cta + warp);
+  // t_gl = L when everything stays on chip.
+  int t_gl, g_rows;
+  std::uint32_t* gscratch;
   int tm_alloc;  // TMEM columns allocated per CTA (power of two)
   std::int64_t safe_stage;  // window start of an interior frame (loads of empty frame slots)
   // IMAD multipliers 1, 2, -1 read from the parameter bank: ptxas cannot
@@ -279,6 +286,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #endif
 #ifndef VD_FAST_TB
 #define VD_FAST_TB 1
+#endif
+#ifndef VD_GLOBAL_SPILL
+#define VD_GLOBAL_SPILL 2  // 1: spill to global rows only when no on-chip layout fits; 2: prefer 12 warps + spill
 #endif
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2
@@ -395,14 +405,18 @@ struct BlockCtx {
   int dummy_row;             // row index receiving out-of-range decision words
   int t_first, t_split;      // TMEM holds stages [t_first, t_split)
   std::uint32_t taddr;       // TMEM address of this warp's column t_first
+  int t_gl;                  // stages [t_gl, L) live in global scratch rows
+  std::uint32_t* grow_lane;  // global scratch rows of this warp slot + lane
 };
 
 // Decision word of stage t -> its survivor slot (TMEM column or smem row).
-template <bool TM>
+template <bool TM, bool GL>
 __device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32_t word) {
   const bool in = t >= bc.v1 && t < bc.L;
   if (TM && in && t < bc.t_split) {
     tmem_st1(bc.taddr + static_cast<std::uint32_t>(t - bc.t_first), word);
+  } else if (GL && in && t >= bc.t_gl) {
+    bc.grow_lane[(t - bc.t_gl) * 32] = word;
   } else {
     bc.drow_lane[(in ? t - bc.s_base : bc.dummy_row) * 32] = word;
   }
@@ -413,7 +427,7 @@ __device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32
 // pending stores all go to shared memory / tensor memory, MODE 4 the same with
 // the target picked at run time (one code copy); MODE 3 blocks lie entirely
 // in the v1 warm-up (ACS only: no decision words, no stores).
-template <class C, class GEO, int MODE, bool TM, int BUF, class RecFn>
+template <class C, class GEO, int MODE, bool TM, bool GL, int BUF, class RecFn>
 __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
                                           const std::uint32_t* pfA, const std::uint32_t* pfB, int pf_room,
                                           RecFn&& rec) {
@@ -492,11 +506,13 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     if constexpr (MODE == 3) continue;
     const std::uint32_t word = compact16(st.wv[(k + 1) & 1]);
     if constexpr (MODE == 0) {
-      store_dec<TM>(bc, tprev, word);
+      store_dec<TM, GL>(bc, tprev, word);
       tprev = t;
       rec(t, k);
     } else if constexpr (MODE == 1) {
       bc.drow_lane[(t - 1 - bc.s_base) * 32] = word;
+    } else if constexpr (MODE == 5) {
+      bc.grow_lane[(t - 1 - bc.t_gl) * 32] = word;  // one coalesced 128-byte row per warp
     } else {
       tw[k] = word;  // one 4-column tensor-memory store per block, below
     }
@@ -517,7 +533,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   if constexpr (MODE != 0) tprev = blk * LB + LB - 1;
 }
 
-template <class C, int R, bool TM>
+template <class C, int R, bool TM, bool GL>
 __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   using GEO = Geo<C, R>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, r = GEO::r, g = GEO::g;
@@ -596,6 +612,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   const int t_split = TM ? static_cast<int>(opaque(static_cast<std::uint32_t>(fp.t_split))) : v1;
   const int t_first = TM ? static_cast<int>(opaque(static_cast<std::uint32_t>(fp.t_first))) : v1;
   const int s_base = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.s_base)));
+  const int t_gl = GL ? static_cast<int>(opaque(static_cast<std::uint32_t>(fp.t_gl))) : L;
   // Frame-relative LLR word pointers (frame start is 4-byte aligned: checked at launch).
   const std::uint32_t* llrA = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
                                                                      (wsA - p.llr_stage0) * B);
@@ -723,6 +740,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   bc.t_first = t_first;
   bc.t_split = t_split;
   // this warp's TMEM lanes (32 * (warp % 4)) and columns (tcols * (warp / 4))
+  bc.t_gl = t_gl;
+  bc.grow_lane = fp.gscratch + (static_cast<std::size_t>(blockIdx.x) * fp.warps_per_cta + warp) *
+                                   static_cast<std::size_t>(fp.g_rows) * 32 + lane;
   bc.taddr = tbase + ((32u * static_cast<std::uint32_t>(warp & 3)) << 16) +
              static_cast<std::uint32_t>(fp.tcols * (warp >> 2));
   int tprev = -1;
@@ -800,15 +820,17 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     const bool clean = (t0 - 1 >= v1) && (t0 + LB - 2 < L) && !(next_rec >= t0 && next_rec < t0 + LB);
     if (t0 + LB <= v1) {
       // warm-up block: every stage (and the next block's pending one) < v1
-      run_block<C, GEO, 3, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    } else if (VD_MERGED_STORE && clean && (t0 - 1 >= t_split || (TM && t0 + LB - 2 < t_split))) {
-      run_block<C, GEO, 4, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    } else if (clean && t0 - 1 >= t_split) {
-      run_block<C, GEO, 1, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+      run_block<C, GEO, 3, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+    } else if (VD_MERGED_STORE && clean && (!GL || t0 + LB - 2 < t_gl) && (t0 - 1 >= t_split || (TM && t0 + LB - 2 < t_split))) {
+      run_block<C, GEO, 4, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+    } else if (GL && clean && t0 - 1 >= t_gl) {
+      run_block<C, GEO, 5, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+    } else if (clean && t0 - 1 >= t_split && (!GL || t0 + LB - 2 < t_gl)) {
+      run_block<C, GEO, 1, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     } else if (TM && clean && t0 + LB - 2 < t_split) {
-      run_block<C, GEO, 2, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+      run_block<C, GEO, 2, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     } else {
-      run_block<C, GEO, 0, TM, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+      run_block<C, GEO, 0, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
     }
     pf_off += WPB;
     pfA += WPB;
@@ -820,7 +842,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     if (blk + 1 < nblk) one_block(blk + 1, std::integral_constant<int, 1>{});
   }
   // decisions of the last processed stage
-  store_dec<TM>(bc, tprev, compact16(st.wv[(nblk * LB - 1) & 1]));
+  store_dec<TM, GL>(bc, tprev, compact16(st.wv[(nblk * LB - 1) & 1]));
   if constexpr (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   __syncwarp();
 
@@ -887,6 +909,40 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
         u = (pn & (R - 1)) | hsh;
       };
       int tb0 = L - LB;
+      if (GL && t_gl < L) {
+        // global scratch rows: a group's G words of a stage are contiguous, so
+        // the loads do not depend on the traced lane and run one block ahead
+        const std::uint32_t* grow = bc.grow_lane - lane + gcol;
+        if constexpr (G == 4) {
+          uint4 cur[LB], nxt[LB];
+#pragma unroll
+          for (int j = 0; j < LB; ++j) cur[j] = *reinterpret_cast<const uint4*>(grow + (tb0 + j - t_gl) * 32);
+          for (; tb0 >= t_gl; tb0 -= LB) {
+            if (tb0 - LB >= t_gl) {
+#pragma unroll
+              for (int j = 0; j < LB; ++j)
+                nxt[j] = *reinterpret_cast<const uint4*>(grow + (tb0 - LB + j - t_gl) * 32);
+            }
+            std::uint32_t wd[LB];
+#pragma unroll
+            for (int j = 0; j < LB; ++j) {
+              const uint4 c = cur[j];
+              const std::uint32_t lo = (lp & 1u) ? c.y : c.x, hi = (lp & 1u) ? c.w : c.z;
+              wd[j] = (lp & 2u) ? hi : lo;
+            }
+            step_block(tb0, wd);
+#pragma unroll
+            for (int j = 0; j < LB; ++j) cur[j] = nxt[j];
+          }
+        } else {
+          for (; tb0 >= t_gl; tb0 -= LB) {
+            std::uint32_t wd[LB];
+#pragma unroll
+            for (int j = 0; j < LB; ++j) wd[j] = grow[(tb0 + j - t_gl) * 32 + lp];
+            step_block(tb0, wd);
+          }
+        }
+      }
       for (; tb0 >= v1 && (!TM || tb0 >= t_split); tb0 -= LB) {  // shared-memory rows
         std::uint32_t wd[LB];
         const std::uint32_t* src = dec + (tb0 - s_base) * 32 + gcol + lp;
@@ -942,6 +998,9 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
         tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
 #pragma unroll
         for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
+      } else if (GL && tb0 >= t_gl) {
+#pragma unroll
+        for (int j = 0; j < LB; ++j) wd[j] = bc.grow_lane[(tb0 + j - t_gl) * 32 - lane + gcol + static_cast<int>(lp)];
       } else {
 #pragma unroll
         for (int j = 0; j < LB; ++j) {
@@ -1059,10 +1118,27 @@ inline SideStream* side_stream() {
   return &(cache.m[dev] = ss);
 }
 
+// The device's default memory pool keeps freed blocks (release threshold =
+// max) so the per-launch cudaMallocAsync of the spill scratch is a pool hit.
+inline cudaError_t scratch_pool() {
+  static std::mutex mu;
+  static std::map<int, bool> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return cudaSuccess;
+  cudaMemPool_t pool;
+  if (cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev); e != cudaSuccess) return e;
+  std::uint64_t thr = ~0ull;
+  if (cudaError_t e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr); e != cudaSuccess) return e;
+  done[dev] = true;
+  return cudaSuccess;
+}
+
 struct Plan {
   FastParams fp;
   std::size_t smem;
-  bool tm;
+  bool tm, gl;
 };
 
 template <class C, int R>
@@ -1123,28 +1199,72 @@ bool plan(const DecodeLaunch& p, Plan* out) {
     int w, alloc;
   };
   const Cand cands[] = {{12, 512}, {8, 512}, {4, 256}};
-  bool ok = false;
-  for (const Cand& c : cands) {
-    const bool last = &c == &cands[2];
-    if (!last && warps_needed < static_cast<std::int64_t>(c.w) * 148) continue;  // would not fill the GPU
+  fp.t_gl = fp.L;  // no global rows unless a spill layout is chosen below
+  fp.g_rows = 0;
+  fp.gscratch = nullptr;
+  // TMEM + smem rows for candidate c; with `spill`, the rows that do not fit in
+  // shared memory go to global scratch (stages [t_gl, L), t_gl % 4 == 0).
+  // Test hook: VITDEC_SPILL_ROWS=N caps the shared-memory rows at N and forces
+  // the spill layout, so small parity tests exercise the global tier.
+  const char* env_rows = std::getenv("VITDEC_SPILL_ROWS");
+  const int cap_rows = env_rows ? std::atoi(env_rows) : -1;
+  auto try_cand = [&](const Cand& c, bool spill) {
     fp.tm_alloc = c.alloc;
     fp.tcols = ((c.alloc / (c.w / 4)) & ~3);
     fp.t_first = p.v1 & ~3;
     fp.t_split = fp.t_first + fp.tcols;
     fp.s_base = fp.t_split;
+    fp.t_gl = fp.L;
+    fp.g_rows = 0;
     layout(std::max(fp.L - fp.t_split, 0) + 1);
-    if (kHeader + static_cast<std::size_t>(fp.smem_per_warp) * c.w <= static_cast<std::size_t>(kSmemMax)) {
+    const bool fits = kHeader + static_cast<std::size_t>(fp.smem_per_warp) * c.w <= static_cast<std::size_t>(kSmemMax);
+    if (fits && (cap_rows < 0 || fp.L - fp.t_split <= cap_rows)) return true;
+    if (!spill) return false;
+    const int budget = (kSmemMax - kHeader) / c.w - x_bytes - ss_bytes - 16;  // bytes of smem rows per warp
+    int rows = budget / 128 - 1;                                               // minus the dummy row
+    if (cap_rows >= 0) rows = std::min(rows, cap_rows);
+    if (rows < 0) return false;
+    fp.t_gl = std::max(fp.t_split, (fp.t_split + rows) & ~3);
+    if (fp.t_gl >= fp.L) return false;
+    fp.g_rows = fp.L - fp.t_gl + 4;  // + 4 rows of padding: the general traceback reads whole blocks
+    layout(fp.t_gl - fp.t_split + 1);
+    return kHeader + static_cast<std::size_t>(fp.smem_per_warp) * c.w <= static_cast<std::size_t>(kSmemMax);
+  };
+  bool ok = false;
+  if ((VD_GLOBAL_SPILL == 2 && warps_needed >= 12 * 148) || cap_rows >= 0) {
+    ok = try_cand(cands[0], true);
+    fp.warps_per_cta = 12;
+  }
+  for (const Cand& c : cands) {
+    if (ok) break;
+    const bool last = &c == &cands[2];
+    if (!last && warps_needed < static_cast<std::int64_t>(c.w) * 148) continue;  // would not fill the GPU
+    if (try_cand(c, false)) {
       fp.warps_per_cta = c.w;
-      out->tm = true;
       ok = true;
-      break;
     }
   }
+  if (!ok && VD_GLOBAL_SPILL) {
+    // Long frames: 12 (or fewer for small launches) warps with TMEM + smem + global rows.
+    for (const Cand& c : cands) {
+      const bool last = &c == &cands[2];
+      if (!last && warps_needed < static_cast<std::int64_t>(c.w) * 148) continue;
+      if (try_cand(c, true)) {
+        fp.warps_per_cta = c.w;
+        ok = true;
+        break;
+      }
+    }
+  }
+  if (ok) out->tm = true;
+  out->gl = ok && fp.g_rows > 0;
   if (!ok) {
     // Long frames: shared memory only, as many warps as fit.
     fp.tcols = 0;
     fp.tm_alloc = 0;
     fp.t_first = fp.t_split = fp.s_base = p.v1;
+    fp.t_gl = fp.L;
+    fp.g_rows = 0;
     layout(p.f + p.v2 + 1);
     const int w = (kSmemMax - kHeader) / fp.smem_per_warp;
     if (w < 1) return false;
@@ -1188,9 +1308,11 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   }
   const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
   std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
-  auto kern = pl.tm ? fast_kernel<C, R, true> : fast_kernel<C, R, false>;
+  auto kern = !pl.tm ? fast_kernel<C, R, false, false>
+                     : pl.gl ? fast_kernel<C, R, true, true> : fast_kernel<C, R, true, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem));
   if (e != cudaSuccess) return e;
+  FastParams fpl = fp;
   // persistent grid: as many CTAs as are co-resident (one per SM with TMEM)
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fp.warps_per_cta * 32, pl.smem) != cudaSuccess ||
@@ -1199,8 +1321,20 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
     per_sm = 1;
   }
   blocks = std::min<std::int64_t>(blocks, static_cast<std::int64_t>(sm_count()) * per_sm);
-  kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fp);
+  if (fp.g_rows > 0) {
+    // stream-ordered scratch for the spilled survivor rows (the pool keeps it
+    // cached across launches, see scratch_pool())
+    const std::size_t bytes = static_cast<std::size_t>(blocks) * fp.warps_per_cta * fp.g_rows * 32 * 4;
+    if (cudaError_t ea = scratch_pool(); ea != cudaSuccess) return ea;
+    if (cudaError_t ea = cudaMallocAsync(reinterpret_cast<void**>(&fpl.gscratch), bytes, stream); ea != cudaSuccess)
+      return ea;
+  }
+  kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fpl);
   e = cudaGetLastError();
+  if (fpl.gscratch) {
+    const cudaError_t ef = cudaFreeAsync(fpl.gscratch, stream);
+    if (e == cudaSuccess) e = ef;
+  }
   if (e == cudaSuccess && edges) e = cudaStreamWaitEvent(stream, side->join, 0);
   return e;
 }

@@ -297,3 +297,62 @@ def test_fast_path_full_int8_range(code, port):
         packed, _ = vd.framed_decode_stream(q, n, t, cfg)
         got = vd.unpack_bits(packed, n)
         assert np.array_equal(got, exp), (code, cfg, np.flatnonzero(got != exp)[:10])
+
+
+@pytest.mark.parametrize("rows", [0, 37])
+@pytest.mark.parametrize("code", [K7, (7, 3, [0o133, 0o171, 0o165]), (9, 2, [0o561, 0o753]), (5, 2, [0o23, 0o35])],
+                         ids=lambda c: f"K{c[0]}B{c[1]}" if isinstance(c, tuple) else str(c))
+def test_global_spill_tier(code, rows, port, monkeypatch):
+    """Survivor rows spilled to global scratch (the long-frame tier): the test
+    hook VITDEC_SPILL_ROWS caps the shared-memory rows so every config below
+    keeps stages [t_gl, L) in global memory; bit-exact vs the oracle."""
+    monkeypatch.setenv("VITDEC_SPILL_ROWS", str(rows))
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng(500 + k + rows)
+    cfgs = [vd.FrameConfig(256, 20, 20), vd.FrameConfig(1024, 42, 42), vd.FrameConfig(320, 20, 45, 32),
+            vd.FrameConfig(500, 26, 51), vd.FrameConfig(384, 20, 40, 64, vd.TracebackStart.kRandom, 9)]
+    for i, cfg in enumerate(cfgs):
+        n = int(rng.integers(80_000, 140_000))
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(1, 4)), 900 + i)
+        q = oracle.quantize(rx, 32.0)
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+        got = vd.unpack_bits(packed, n)
+        bad = np.flatnonzero(got != exp)
+        assert bad.size == 0, (k, rows, cfg, n, bad[:10], bad.size)
+        assert (stats.frames, stats.stages, stats.tracebacks) == st
+
+
+def test_long_frames_full_size_sampled_windows(port):
+    """f = 1024 at 2^25 stages (a full-GPU launch: the natural spill layout,
+    12 warps per SM with TMEM + smem + global rows): sampled frame windows
+    re-decoded by the oracle are bit-identical; BER sane."""
+    import torch
+
+    from paper_2011_09337_b200.device import count_bit_errors, decode_i8_device, synth_llr_i8
+
+    t = trellis(*K7)
+    n = 1 << 25
+    for cfg in (vd.FrameConfig(1024, 42, 42), vd.FrameConfig(512, 20, 63)):
+        f, v1, v2 = cfg.f, cfg.v1, cfg.v2
+        llr = torch.empty(n * 2, dtype=torch.int8, device="cuda")
+        bits = torch.empty(n // 32, dtype=torch.int32, device="cuda")
+        out = torch.empty(n // 32 + 1, dtype=torch.int32, device="cuda")
+        synth_llr_i8(t, n, 0.7, 32.0, 4321, llr, bits)
+        decode_i8_device(t, cfg, n, llr, 0, 0, -(-n // f), out, 0)
+        cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
+        count_bit_errors(out, bits, n, cnt)
+        torch.cuda.synchronize()
+        assert int(cnt.item()) < n * 2e-3
+        got_all = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
+        q = llr.cpu().numpy()
+        rng = np.random.default_rng(f)
+        nf = n // f
+        for m0 in list(rng.integers(1, nf - 8, 6)) + [0, nf - 4]:
+            m1 = min(m0 + 4, nf)
+            g0 = max(m0 - (-(-v1 // f)), 0)  # window origin on the frame grid
+            lo, hi = g0 * f, min(m1 * f + v2, n)
+            exp, _, _ = port.framed_decode(*K7, q[lo * 2:hi * 2], hi - lo, f, v1, v2)
+            a, b2 = (m0 - g0) * f, (m1 - g0) * f
+            assert np.array_equal(got_all[m0 * f:m1 * f], exp[a:b2]), (cfg, m0)
