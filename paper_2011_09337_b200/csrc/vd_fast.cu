@@ -290,6 +290,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_GLOBAL_SPILL
 #define VD_GLOBAL_SPILL 2  // 1: spill to global rows only when no on-chip layout fits; 2: prefer 12 warps + spill
 #endif
+#ifndef VD_DEC_FORM
+#define VD_DEC_FORM 2  // measured +1 % over the CN-table form (profiles/r01_ab_notes.md)
+#endif
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2
 #endif
@@ -335,6 +338,7 @@ struct FrameState {
   std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : 3];
   std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
   std::uint32_t one, two, m1;         // opaque 1, 2, -1 (IMAD multipliers)
+  std::uint32_t two_p;                // 2 from the parameter bank (not constant-folded by ptxas)
 };
 
 // Branch tables of one block: PT[k][x] = T_k[x ^ lane part] + 128 B per half
@@ -440,10 +444,13 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   // CN[k][x] = PT[x] - PT[x ^ XM] + 0x7FFF per half = 2 PT[x] - OFFB + 0x7FFF7FFF.
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * GEO::B) * 0x00010001u;
   std::uint32_t CN[LB][1 << GEO::B];
+  (void)CN;
+  if constexpr (VD_DEC_FORM == 1) {
 #pragma unroll
-  for (int k = 0; k < LB; ++k) {
+    for (int k = 0; k < LB; ++k) {
 #pragma unroll
-    for (int x = 0; x < (1 << GEO::B); ++x) CN[k][x] = mad_u32(PT[k][x], st.two, 0x7fff7fffu - OFFB);
+      for (int x = 0; x < (1 << GEO::B); ++x) CN[k][x] = mad_u32(PT[k][x], st.two, 0x7fff7fffu - OFFB);
+    }
   }
   // The words of this buffer are consumed: refill it with block blk + 2 now,
   // so two full blocks of work cover the HBM latency.
@@ -490,9 +497,17 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       if constexpr (MODE == 3) {
       } else if (pair < kFmaPairs) {
         // FMA-pipe form: (sE - sO) + (PT[x] - PT[x ^ XM] + 0x7FFF), 3 IMAD per pair
-        const std::uint32_t d = mad_u32(sO, st.m1, sE);
-        w[e] = mad_u32(d, st.one, CN[k][x]);
-        w[od] = mad_u32(d, st.one, CN[k][x ^ XM]);
+        if constexpr (VD_DEC_FORM == 2) {
+          // d' = sE - sO + 0x7FFF - OFFB per half (one IADD3), then 2 PT + d' as
+          // IMADs with a multiplier ptxas cannot see (no CN tables)
+          const std::uint32_t dp = sE - sO + (0x7fff7fffu - OFFB);
+          w[e] = mad_u32(PT[k][x], st.two_p, dp);
+          w[od] = mad_u32(PT[k][x ^ XM], st.two_p, dp);
+        } else {
+          const std::uint32_t d = mad_u32(sO, st.m1, sE);
+          w[e] = mad_u32(d, st.one, CN[k][x]);
+          w[od] = mad_u32(d, st.one, CN[k][x ^ XM]);
+        }
       } else {
         // ALU-pipe form: new - s2 (>= 0, 0 iff the second won) + 0x7FFF, 1 IADD3 each
         w[e] = nL - s2L + 0x7fff7fffu;
@@ -647,6 +662,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
 #pragma unroll
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
   }
+  st.two_p = fp.two;
 #if VD_PARAM_MULS
   st.one = fp.one;
   st.two = fp.two;
