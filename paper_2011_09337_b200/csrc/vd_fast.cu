@@ -236,6 +236,12 @@ struct FastParams {
   // t_gl = L when everything stays on chip.
   int t_gl, g_rows;
   std::uint32_t* gscratch;
+  // Head frames (window start m*f - v1 < 0, clipped by the stream start) read
+  // a zero-padded copy of the stream head: llr_head[(t + v1) * B] = stage t,
+  // zero for t < 0. All-zero branch metrics keep every path metric at 0, so
+  // v1 padded stages leave sigma = 0 at stage 0 exactly as the clipped window
+  // starts (reference decoder.cpp:195), and the traceback stops at stage 0.
+  const std::int8_t* llr_head;
   int tm_alloc;  // TMEM columns allocated per CTA (power of two)
   std::int64_t safe_stage;  // window start of an interior frame (loads of empty frame slots)
   // IMAD multipliers 1, 2, -1 read from the parameter bank: ptxas cannot
@@ -292,6 +298,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #endif
 #ifndef VD_DEC_FORM
 #define VD_DEC_FORM 2  // measured +1 % over the CN-table form (profiles/r01_ab_notes.md)
+#endif
+#ifndef VD_PAD_HEAD
+#define VD_PAD_HEAD 1
 #endif
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2
@@ -629,10 +638,13 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   const int s_base = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.s_base)));
   const int t_gl = GL ? static_cast<int>(opaque(static_cast<std::uint32_t>(fp.t_gl))) : L;
   // Frame-relative LLR word pointers (frame start is 4-byte aligned: checked at launch).
-  const std::uint32_t* llrA = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
-                                                                     (wsA - p.llr_stage0) * B);
-  const std::uint32_t* llrB = reinterpret_cast<const std::uint32_t*>(static_cast<const std::int8_t*>(p.llr) +
-                                                                     (wsB - p.llr_stage0) * B);
+  auto llr_of = [&](std::int64_t ws) {
+    const std::int8_t* b8 = (fp.llr_head != nullptr && ws < 0) ? fp.llr_head + (ws + p.v1) * B
+                                                               : static_cast<const std::int8_t*>(p.llr) + (ws - p.llr_stage0) * B;
+    return reinterpret_cast<const std::uint32_t*>(b8);
+  };
+  const std::uint32_t* llrA = llr_of(wsA);
+  const std::uint32_t* llrB = llr_of(wsB);
 
   FrameState<GEO> st;
   // Per-phase flip constants for this lane (lane part of the branch index).
@@ -1158,9 +1170,10 @@ struct Plan {
 };
 
 template <class C, int R>
-bool plan(const DecodeLaunch& p, Plan* out) {
+bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   using GEO = Geo<C, R>;
   FastParams fp{};
+  fp.llr_head = nullptr;
   fp.p = p;
   fp.one = 1u;
   fp.two = 2u;
@@ -1184,7 +1197,7 @@ bool plan(const DecodeLaunch& p, Plan* out) {
     if (p.frame_list || p.sigma) return false;
   } else {
   const std::int64_t span = static_cast<std::int64_t>(fp.L) + 4;  // stages read per frame (word granularity slack)
-  std::int64_t lo = (p.v1 + p.f - 1) / p.f;                                    // first m with m*f >= v1
+  std::int64_t lo = pad_head ? p.frame_begin : (p.v1 + p.f - 1) / p.f;  // first m with m*f >= v1 (or padded head)
   std::int64_t hi_excl = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // m*f + f + v2 <= n
   // the caller guarantees LLRs up to the window end of the last launched frame
   const std::int64_t avail = std::min<std::int64_t>(p.frame_end * static_cast<std::int64_t>(p.f) + p.v2, p.n);
@@ -1194,7 +1207,7 @@ bool plan(const DecodeLaunch& p, Plan* out) {
   fp.mi1 = hi_excl < p.frame_end ? hi_excl : p.frame_end;
   if (fp.mi1 - fp.mi0 < GEO::FPW) return false;  // not worth it
   // also the llr window must start at or before the first interior frame's beg
-  if (p.llr_stage0 > fp.mi0 * p.f - p.v1) return false;
+  if (!pad_head && p.llr_stage0 > fp.mi0 * p.f - p.v1) return false;
   fp.safe_stage = fp.mi0 * p.f - p.v1;
   }
   const int x_bytes = GEO::g > 0 ? GEO::GROUPS * GEO::XSTRIDE * 4 : 0;
@@ -1296,7 +1309,27 @@ template <class C, int R>
 cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   using GEO = Geo<C, R>;
   Plan pl;
-  if (!plan<C, R>(p, &pl)) return cudaErrorNotSupported;
+  // Head frames on the fast path via a zero-padded copy of the stream head
+  // (exact, see FastParams::llr_head); otherwise they go to the generic kernel.
+  const std::int64_t head_end = std::min<std::int64_t>((p.v1 + p.f - 1) / p.f, p.frame_end);
+  bool pad = VD_PAD_HEAD && p.nblocks == 0 && p.llr_stage0 == 0 && p.frame_begin < head_end &&
+             plan<C, R>(p, &pl, true) && pl.fp.mi0 == p.frame_begin && pl.fp.mi1 >= head_end;
+  if (!pad && !plan<C, R>(p, &pl)) return cudaErrorNotSupported;
+  std::int8_t* head_buf = nullptr;
+  if (pad) {
+    constexpr int B = GEO::B;
+    const std::int64_t stages = head_end * p.f + p.v2;  // window end of the last head frame (<= n: mi1 >= head_end)
+    if (cudaError_t e = scratch_pool(); e != cudaSuccess) return e;
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), (p.v1 + stages) * B, stream);
+        e != cudaSuccess)
+      return e;
+    if (cudaError_t e = cudaMemsetAsync(head_buf, 0, static_cast<std::size_t>(p.v1) * B, stream); e != cudaSuccess)
+      return e;
+    if (cudaError_t e = cudaMemcpyAsync(head_buf + p.v1 * B, p.llr, stages * B, cudaMemcpyDeviceToDevice, stream);
+        e != cudaSuccess)
+      return e;
+    pl.fp.llr_head = head_buf;
+  }
   const FastParams& fp = pl.fp;
   // Edge frames (clipped windows) go to the generic kernel on a side stream,
   // concurrently with the fast kernel (they fit beside its CTA on an SM).
@@ -1349,6 +1382,10 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   e = cudaGetLastError();
   if (fpl.gscratch) {
     const cudaError_t ef = cudaFreeAsync(fpl.gscratch, stream);
+    if (e == cudaSuccess) e = ef;
+  }
+  if (head_buf) {
+    const cudaError_t ef = cudaFreeAsync(head_buf, stream);
     if (e == cudaSuccess) e = ef;
   }
   if (e == cudaSuccess && edges) e = cudaStreamWaitEvent(stream, side->join, 0);
