@@ -302,6 +302,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_PAD_HEAD
 #define VD_PAD_HEAD 1
 #endif
+#ifndef VD_RENORM_TABLE
+#define VD_RENORM_TABLE 1
+#endif
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2
 #endif
@@ -348,6 +351,7 @@ struct FrameState {
   std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
   std::uint32_t one, two, m1;         // opaque 1, 2, -1 (IMAD multipliers)
   std::uint32_t two_p;                // 2 from the parameter bank (not constant-folded by ptxas)
+  std::uint32_t corr;                 // pending renormalisation (BASE - ref per half), VD_RENORM_TABLE
 };
 
 // Branch tables of one block: PT[k][x] = T_k[x ^ lane part] + 128 B per half
@@ -449,6 +453,16 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   // ---- branch-metric tables for the LB stages of this block (both frames) ---
   std::uint32_t PT[LB][1 << GEO::B];
   block_tables<C, GEO, BUF>(st, PT);
+  // Renormalisation folded into the ACS tables (VD_RENORM_TABLE): the block
+  // after a renorm point adds st.corr = BASE - ref per half to its stage-0
+  // ACS tables, which subtracts ref - BASE from every new metric (one
+  // VIADD.16x2 per table entry instead of one IADD3 per state register).
+  // Decision words keep the unshifted tables: both candidates shift equally.
+  constexpr bool CORR = VD_RENORM_TABLE && VD_RENORM_EVERY == 2 && BUF == 0;
+  std::uint32_t PA0[1 << GEO::B];
+#pragma unroll
+  for (int x = 0; x < (1 << GEO::B); ++x) PA0[x] = CORR ? __vadd2(PT[0][x], st.corr) : PT[0][x];
+  auto pa = [&](int k, std::uint32_t x) { return (CORR && k == 0) ? PA0[x] : PT[k][x]; };
   // Decision-word tables of the FMA-pipe form (see the ACS below):
   // CN[k][x] = PT[x] - PT[x ^ XM] + 0x7FFF per half = 2 PT[x] - OFFB + 0x7FFF7FFF.
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * GEO::B) * 0x00010001u;
@@ -494,10 +508,10 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       const int od = e | (1 << k);
       const std::uint32_t x = GEO::xreg(k, e);
       const std::uint32_t sE = st.sig[e], sO = st.sig[od];
-      const std::uint32_t s2L = __vadd2(sO, PT[k][x ^ XM]);
-      const std::uint32_t s2H = __vadd2(sO, PT[k][x]);
-      const std::uint32_t nL = __viaddmax_s16x2(sE, PT[k][x], s2L);
-      const std::uint32_t nH = __viaddmax_s16x2(sE, PT[k][x ^ XM], s2H);
+      const std::uint32_t s2L = __vadd2(sO, pa(k, x ^ XM));
+      const std::uint32_t s2H = __vadd2(sO, pa(k, x));
+      const std::uint32_t nL = __viaddmax_s16x2(sE, pa(k, x), s2L);
+      const std::uint32_t nH = __viaddmax_s16x2(sE, pa(k, x ^ XM), s2H);
       // Decision words: bit 15 / 31 set iff the FIRST predecessor won, i.e.
       // s1 - s2 >= 1 per half (ties -> second, decoder.cpp:67-74); + 0x7FFF
       // per half keeps each half in [0, 0xFFFE], so no carry crosses halves.
@@ -675,6 +689,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
   }
   st.two_p = fp.two;
+  st.corr = 0u;
 #if VD_PARAM_MULS
   st.one = fp.one;
   st.two = fp.two;
@@ -790,8 +805,12 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
       const std::uint32_t ref = __shfl_sync(kFull, st.sig[0], grp * G);
       subA += static_cast<std::int32_t>(ref & 0xffffu) - 8192;
       subB += static_cast<std::int32_t>(ref >> 16) - 8192;
+      if constexpr (VD_RENORM_TABLE && VD_RENORM_EVERY == 2) {
+        st.corr = __vsub2(BASE, ref);  // applied by the next (BUF 0) block's stage-0 tables
+      } else {
 #pragma unroll
-      for (int i = 0; i < R; ++i) st.sig[i] = st.sig[i] - ref + BASE;
+        for (int i = 0; i < R; ++i) st.sig[i] = st.sig[i] - ref + BASE;
+      }
     }
     // ---- relayout: back to the canonical layout (P_new = rotr(P_old, r)) --
     if constexpr (GEO::kChunked) {
