@@ -8,6 +8,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -306,9 +307,13 @@ vd_status decode_device(const vd_code* code, const vd_frame_cfg* cfg, std::int64
 
 void batch_stats(const vd_frame_cfg* cfg, std::int32_t nblocks, const std::int64_t* lens, vd_stats* st) {
   st->frames = st->stages = st->tracebacks = 0;
+  std::int64_t last_len = -1;
+  vd_stats b{};
   for (std::int32_t j = 0; j < nblocks; ++j) {
-    vd_stats b{};
-    vd_frame_stats(cfg, lens[j], &b);
+    if (lens[j] != last_len) {  // BER-sweep batches repeat one block length
+      vd_frame_stats(cfg, lens[j], &b);
+      last_len = lens[j];
+    }
     st->frames += b.frames;
     st->stages += b.stages;
     st->tracebacks += b.tracebacks;
@@ -367,6 +372,21 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
   std::vector<std::int32_t> ilo(nblocks, 0), ihi(nblocks, 0);
   std::vector<std::int64_t> edges;
   std::int64_t safe = -1, interior = 0;
+  // Edge frames the fast kernel can still take (int8 path): HEAD frames
+  // (window clipped at the block start, full right window) read a zero-padded
+  // copy of their block head — all-zero branch metrics keep sigma = 0 until
+  // stage 0 — and TAIL frames with a full output but a clipped right overlap
+  // v2' < v2 are exactly frames of configuration (f, v1, v2') (one traceback
+  // per frame: the start stage is the window end either way), one launch per
+  // distinct v2'. Everything else goes to the generic kernel.
+  const std::int64_t head_end = (v1 + f - 1) / f;
+  const bool one_tb = cfg->f0 == 0 || cfg->f0 >= f;
+  // test / A-B hooks: VITDEC_BATCH_EDGES=generic keeps every edge frame on the generic kernel
+  const char* env_edges = std::getenv("VITDEC_BATCH_EDGES");
+  const int edge_mode = !env_edges ? 3 : std::strcmp(env_edges, "generic") == 0 ? 0
+                        : std::strcmp(env_edges, "heads") == 0 ? 1 : std::strcmp(env_edges, "tails") == 0 ? 2 : 3;
+  std::vector<std::int64_t> heads;
+  std::map<int, std::vector<std::int64_t>> tails;  // v2' -> global frame ids
   for (std::int32_t j = 0; j < nblocks; ++j) {
     std::int64_t lo = 0, hi = 0;
     if (fast && (bstage[j] * B) % 4 == 0) {
@@ -381,8 +401,19 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
     ihi[j] = static_cast<std::int32_t>(hi);
     if (hi > lo && safe < 0) safe = bstage[j] + lo * f - v1;
     interior += hi - lo;
-    for (std::int64_t m = 0; m < bframe[j + 1] - bframe[j]; ++m) {
-      if (m < lo || m >= hi) edges.push_back(bframe[j] + m);
+    const std::int64_t nfj = bframe[j + 1] - bframe[j];
+    for (std::int64_t m = 0; m < nfj; ++m) {
+      if (m == lo && hi > lo) m = hi;  // skip the interior run (the fast kernel's)
+      if (m >= nfj) break;
+      const bool aligned = fast && (bstage[j] * B) % 4 == 0;
+      if ((edge_mode & 1) && aligned && m < head_end && m * f + f + v2 <= lens[j]) {
+        heads.push_back(bframe[j] + m);
+      } else if ((edge_mode & 2) && aligned && one_tb && m >= head_end && m * f + f <= lens[j] && m * f + f + v2 > lens[j] &&
+                 f + v1 + (lens[j] - m * f - f) >= 16) {
+        tails[static_cast<int>(lens[j] - m * f - f)].push_back(bframe[j] + m);
+      } else {
+        edges.push_back(bframe[j] + m);
+      }
     }
   }
 
@@ -396,17 +427,40 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
 
   // Stream-ordered scratch for the tables (freed after the launches).
   const std::size_t nb1 = static_cast<std::size_t>(nblocks) + 1;
-  const std::size_t bytes = sizeof(std::int64_t) * (2 * nb1 + edges.size()) + sizeof(std::int32_t) * 2 * nb1;
-  std::vector<unsigned char> host(bytes);
-  std::memcpy(host.data(), bstage.data(), sizeof(std::int64_t) * nb1);
-  std::memcpy(host.data() + sizeof(std::int64_t) * nb1, bframe.data(), sizeof(std::int64_t) * nb1);
-  std::memcpy(host.data() + sizeof(std::int64_t) * 2 * nb1, edges.data(), sizeof(std::int64_t) * edges.size());
-  const std::size_t i32_off = sizeof(std::int64_t) * (2 * nb1 + edges.size());
-  std::memcpy(host.data() + i32_off, ilo.data(), sizeof(std::int32_t) * nblocks);
-  std::memcpy(host.data() + i32_off + sizeof(std::int32_t) * nb1, ihi.data(), sizeof(std::int32_t) * nblocks);
+  // frame lists: generic edges, then heads, then every tail class
+  std::vector<std::int64_t> lists = edges;
+  const std::size_t heads_off = lists.size();
+  lists.insert(lists.end(), heads.begin(), heads.end());
+  std::vector<std::pair<int, std::size_t>> tail_off;  // (v2', offset)
+  for (auto& kv : tails) {
+    tail_off.emplace_back(kv.first, lists.size());
+    lists.insert(lists.end(), kv.second.begin(), kv.second.end());
+  }
+  const std::size_t bytes = sizeof(std::int64_t) * (2 * nb1 + lists.size()) + sizeof(std::int32_t) * 2 * nb1;
+  // pinned staging (per host thread, grows) so the table upload is a true async copy
+  thread_local unsigned char* pinned = nullptr;
+  thread_local std::size_t pinned_cap = 0;
+  thread_local cudaEvent_t pinned_done = nullptr;  // last upload out of the staging buffer
+  if (pinned_done) VD_CUDA(cudaEventSynchronize(pinned_done), "batch table staging");
+  if (pinned_cap < bytes) {
+    if (pinned) cudaFreeHost(pinned);
+    pinned = nullptr;
+    pinned_cap = 0;
+    VD_CUDA(cudaMallocHost(reinterpret_cast<void**>(&pinned), bytes), "cudaMallocHost(batch tables)");
+    pinned_cap = bytes;
+  }
+  unsigned char* host_p = pinned;
+  std::memcpy(host_p, bstage.data(), sizeof(std::int64_t) * nb1);
+  std::memcpy(host_p + sizeof(std::int64_t) * nb1, bframe.data(), sizeof(std::int64_t) * nb1);
+  std::memcpy(host_p + sizeof(std::int64_t) * 2 * nb1, lists.data(), sizeof(std::int64_t) * lists.size());
+  const std::size_t i32_off = sizeof(std::int64_t) * (2 * nb1 + lists.size());
+  std::memcpy(host_p + i32_off, ilo.data(), sizeof(std::int32_t) * nblocks);
+  std::memcpy(host_p + i32_off + sizeof(std::int32_t) * nb1, ihi.data(), sizeof(std::int32_t) * nblocks);
   unsigned char* dscratch = nullptr;
   VD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dscratch), bytes, s), "cudaMallocAsync(batch tables)");
-  VD_CUDA(cudaMemcpyAsync(dscratch, host.data(), bytes, cudaMemcpyHostToDevice, s), "upload batch tables");
+  VD_CUDA(cudaMemcpyAsync(dscratch, host_p, bytes, cudaMemcpyHostToDevice, s), "upload batch tables");
+  if (!pinned_done) VD_CUDA(cudaEventCreateWithFlags(&pinned_done, cudaEventDisableTiming), "cudaEventCreate");
+  VD_CUDA(cudaEventRecord(pinned_done, s), "cudaEventRecord");
   p.nblocks = nblocks;
   p.blk_stage = reinterpret_cast<const std::int64_t*>(dscratch);
   p.blk_frame = p.blk_stage + nb1;
@@ -417,6 +471,8 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
   VD_CUDA(cudaMemsetAsync(out, 0, sizeof(std::uint32_t) * ((n_total + 31) / 32), s), "zero output");
   cudaError_t e = cudaSuccess;
   bool fast_launched = false;
+  std::int64_t* extra_list = nullptr;
+  std::int8_t* head_buf = nullptr;
   if (fast && interior > 0) {
     vd::DecodeLaunch q = p;
     q.frame_begin = 0;
@@ -427,12 +483,64 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
       fast_launched = true;
     }
   }
+  // head and tail classes on the fast kernel (frame-list launches)
+  std::vector<std::int64_t> back_to_generic;
+  if constexpr (sizeof(T) == 1) {
+    if (e == cudaSuccess && fast_launched && !heads.empty()) {
+      const std::int64_t pitch = (v1 + head_end * f + v2 + 3) & ~std::int64_t(3);  // 4-byte aligned block heads
+      e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), static_cast<std::size_t>(pitch) * B * nblocks + 16, s);
+      if (e == cudaSuccess)
+        e = vd::launch_head_gather(reinterpret_cast<const std::int8_t*>(llr), p.blk_stage, nblocks, B, v1, pitch,
+                                   head_end * f + v2, head_buf, s);
+      vd::DecodeLaunch q = p;
+      q.frame_list = dedges + heads_off;
+      q.frame_begin = 0;
+      q.frame_end = static_cast<std::int64_t>(heads.size());
+      q.safe_stage = safe;
+      q.llr_head = head_buf;
+      q.head_pitch = pitch;
+      if (e == cudaSuccess) {
+        if (vd::fast_path_supported(q)) {
+          e = vd::launch_fast_i8(q, s);
+        } else {
+          back_to_generic.insert(back_to_generic.end(), heads.begin(), heads.end());
+        }
+      }
+    } else if (!heads.empty()) {
+      back_to_generic.insert(back_to_generic.end(), heads.begin(), heads.end());
+    }
+    for (const auto& to : tail_off) {
+      const std::vector<std::int64_t>& lst = tails[to.first];
+      vd::DecodeLaunch q = p;
+      q.v2 = to.first;
+      q.frame_list = dedges + to.second;
+      q.frame_begin = 0;
+      q.frame_end = static_cast<std::int64_t>(lst.size());
+      q.safe_stage = safe;
+      if (e == cudaSuccess && fast_launched && vd::fast_path_supported(q)) {
+        e = vd::launch_fast_i8(q, s);
+      } else {
+        back_to_generic.insert(back_to_generic.end(), lst.begin(), lst.end());
+      }
+    }
+  }
   if (e == cudaSuccess) {
     vd::DecodeLaunch q = p;
     q.frame_begin = 0;
-    if (fast_launched) {
+    if (fast_launched && back_to_generic.empty()) {
       q.frame_list = dedges;
       q.frame_end = static_cast<std::int64_t>(edges.size());
+    } else if (fast_launched) {
+      // rare: a head / tail class the fast kernel declined; decode the whole
+      // remaining list (edges + declined frames) with the generic kernel
+      std::vector<std::int64_t> all = edges;
+      all.insert(all.end(), back_to_generic.begin(), back_to_generic.end());
+      std::int64_t* dl = nullptr;
+      VD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dl), sizeof(std::int64_t) * all.size(), s), "cudaMallocAsync");
+      VD_CUDA(cudaMemcpyAsync(dl, all.data(), sizeof(std::int64_t) * all.size(), cudaMemcpyHostToDevice, s), "H2D");
+      q.frame_list = dl;
+      q.frame_end = static_cast<std::int64_t>(all.size());
+      extra_list = dl;
     } else {
       q.frame_end = nf_total;
     }
@@ -444,6 +552,8 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
       }
     }
   }
+  if (extra_list) cudaFreeAsync(extra_list, s);
+  if (head_buf) cudaFreeAsync(head_buf, s);
   const cudaError_t ef = cudaFreeAsync(dscratch, s);
   if (e == cudaErrorInvalidValue) return fail(VD_EUNSUPPORTED, "frame configuration exceeds the GPU kernel's shared-memory envelope");
   if (e != cudaSuccess) return cuda_fail(e, "batched decode launch");

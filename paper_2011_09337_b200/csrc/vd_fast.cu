@@ -242,6 +242,7 @@ struct FastParams {
   // v1 padded stages leave sigma = 0 at stage 0 exactly as the clipped window
   // starts (reference decoder.cpp:195), and the traceback stops at stage 0.
   const std::int8_t* llr_head;
+  std::int64_t head_pitch;  // stages per block in llr_head (batched: v1 + head window)
   int tm_alloc;  // TMEM columns allocated per CTA (power of two)
   std::int64_t safe_stage;  // window start of an interior frame (loads of empty frame slots)
   // IMAD multipliers 1, 2, -1 read from the parameter bank: ptxas cannot
@@ -631,14 +632,23 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   // LLRs and write nothing.
   struct Slot {
     std::int64_t ws, m;  // window start stage (stream), block-local frame index
+    int blk;             // block (batched mode)
+    bool head;           // window clipped at the block start: read the zero-padded head copy
   };
+  // Empty slots read some valid window and write nothing: block 0's padded
+  // head when there is one (safe_stage may then be negative), else safe_stage.
+  const Slot empty = fp.llr_head ? Slot{-static_cast<std::int64_t>(p.v1), 0, 0, true} : Slot{fp.safe_stage, 0, 0, false};
   auto frame_slot = [&](std::int64_t mg, bool& valid) -> Slot {
-    if (!valid) return Slot{fp.safe_stage, 0};
+    if (!valid) return empty;
     const FrameRef r = resolve_frame(p, mg);
-    if (p.nblocks > 0) valid = r.m >= __ldg(p.blk_ilo + r.blk) && r.m < __ldg(p.blk_ihi + r.blk);
-    return valid ? Slot{r.base + r.m * p.f - p.v1, r.m} : Slot{fp.safe_stage, 0};
+    // batched main launch: only the block's interior frames (a frame list
+    // launch takes every listed frame)
+    if (p.nblocks > 0 && !p.frame_list) valid = r.m >= __ldg(p.blk_ilo + r.blk) && r.m < __ldg(p.blk_ihi + r.blk);
+    if (!valid) return empty;
+    return Slot{r.base + r.m * p.f - p.v1, r.m, r.blk, fp.llr_head != nullptr && r.m * p.f < p.v1};
   };
-  const std::int64_t wsA = frame_slot(mA, validA).ws, wsB = frame_slot(mB, validB).ws;
+  const Slot slA = frame_slot(mA, validA), slB = frame_slot(mB, validB);
+  const std::int64_t wsA = slA.ws, wsB = slB.ws;
 
   const int f = static_cast<int>(opaque(static_cast<std::uint32_t>(p.f)));
   const int v1 = static_cast<int>(opaque(static_cast<std::uint32_t>(p.v1)));
@@ -652,13 +662,14 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
   const int s_base = static_cast<int>(opaque(static_cast<std::uint32_t>(fp.s_base)));
   const int t_gl = GL ? static_cast<int>(opaque(static_cast<std::uint32_t>(fp.t_gl))) : L;
   // Frame-relative LLR word pointers (frame start is 4-byte aligned: checked at launch).
-  auto llr_of = [&](std::int64_t ws) {
-    const std::int8_t* b8 = (fp.llr_head != nullptr && ws < 0) ? fp.llr_head + (ws + p.v1) * B
-                                                               : static_cast<const std::int8_t*>(p.llr) + (ws - p.llr_stage0) * B;
+  auto llr_of = [&](const Slot& sl) {
+    const std::int8_t* b8 =
+        sl.head ? fp.llr_head + (static_cast<std::int64_t>(sl.blk) * fp.head_pitch + sl.m * p.f) * B
+                : static_cast<const std::int8_t*>(p.llr) + (sl.ws - p.llr_stage0) * B;
     return reinterpret_cast<const std::uint32_t*>(b8);
   };
-  const std::uint32_t* llrA = llr_of(wsA);
-  const std::uint32_t* llrB = llr_of(wsB);
+  const std::uint32_t* llrA = llr_of(slA);
+  const std::uint32_t* llrB = llr_of(slB);
 
   FrameState<GEO> st;
   // Per-phase flip constants for this lane (lane part of the branch index).
@@ -1192,7 +1203,8 @@ template <class C, int R>
 bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   using GEO = Geo<C, R>;
   FastParams fp{};
-  fp.llr_head = nullptr;
+  fp.llr_head = p.llr_head;
+  fp.head_pitch = p.head_pitch;
   fp.p = p;
   fp.one = 1u;
   fp.two = 2u;
@@ -1213,7 +1225,7 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
     fp.mi0 = p.frame_begin;
     fp.mi1 = p.frame_end;
     fp.safe_stage = p.safe_stage;
-    if (p.frame_list || p.sigma) return false;
+    if (p.sigma) return false;
   } else {
   const std::int64_t span = static_cast<std::int64_t>(fp.L) + 4;  // stages read per frame (word granularity slack)
   std::int64_t lo = pad_head ? p.frame_begin : (p.v1 + p.f - 1) / p.f;  // first m with m*f >= v1 (or padded head)
@@ -1339,7 +1351,8 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
     constexpr int B = GEO::B;
     const std::int64_t stages = head_end * p.f + p.v2;  // window end of the last head frame (<= n: mi1 >= head_end)
     if (cudaError_t e = scratch_pool(); e != cudaSuccess) return e;
-    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), (p.v1 + stages) * B, stream);
+    // (+16 bytes: the last LLR word of a window may extend past the window's last stage)
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), (p.v1 + stages) * B + 16, stream);
         e != cudaSuccess)
       return e;
     if (cudaError_t e = cudaMemsetAsync(head_buf, 0, static_cast<std::size_t>(p.v1) * B, stream); e != cudaSuccess)
@@ -1420,7 +1433,34 @@ bool try_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
   return true;
 }
 
+__global__ void head_gather_kernel(const std::int8_t* __restrict__ llr, const std::int64_t* __restrict__ blk_stage,
+                                   int nblocks, int b, int v1, std::int64_t pitch, std::int64_t copy,
+                                   std::int8_t* __restrict__ head) {
+  const std::int64_t pb = pitch * b, total = pb * nblocks;
+  for (std::int64_t i = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t j = i / pb, o = i - j * pb - static_cast<std::int64_t>(v1) * b;
+    std::int8_t v = 0;
+    if (o >= 0) {
+      const std::int64_t s0 = __ldg(blk_stage + j), nj = __ldg(blk_stage + j + 1) - s0;
+      if (o < (copy < nj ? copy : nj) * b) v = llr[s0 * b + o];
+    }
+    head[i] = v;
+  }
+}
+
 }  // namespace fast
+
+cudaError_t launch_head_gather(const std::int8_t* llr, const std::int64_t* blk_stage, int nblocks, int b, int v1,
+                               std::int64_t pitch, std::int64_t copy, std::int8_t* head, cudaStream_t stream) {
+  const std::int64_t total = pitch * b * nblocks;
+  const std::int64_t cap = static_cast<std::int64_t>(sm_count()) * 8;
+  const std::int64_t grid = std::min<std::int64_t>((total + 255) / 256, cap);
+  if (grid <= 0) return cudaSuccess;
+  fast::head_gather_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(llr, blk_stage, nblocks, b, v1, pitch,
+                                                                            copy, head);
+  return cudaGetLastError();
+}
 
 bool fast_path_supported(const DecodeLaunch& p) {
   using namespace fast;

@@ -39,6 +39,11 @@ struct DecodeLaunch {
   // frame ids) instead of the index range itself.
   const std::int64_t* frame_list = nullptr;
   std::int64_t safe_stage = 0;  // batched fast launch: window start of some interior frame
+  // Fast kernel only: frames whose window is clipped by their block start
+  // (m*f < v1) read a zero-padded copy of the block head instead:
+  // llr_head[(blk * head_pitch + (t + v1)) * b] = stage t of block blk.
+  const std::int8_t* llr_head = nullptr;
+  std::int64_t head_pitch = 0;
 };
 
 /// A global frame id resolved to its block: block-local frame index, block
@@ -75,6 +80,11 @@ cudaError_t launch_generic_f64(const DecodeLaunch& p, cudaStream_t stream);
 /// code/config is outside its envelope (caller then uses the generic one).
 bool fast_path_supported(const DecodeLaunch& p);
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream);
+/// Zero-padded block heads for the fast kernel: for every block j of the
+/// batch (blk_stage: device [nblocks + 1]), head[j * pitch * b ...] = v1 zero
+/// stages followed by the block's first min(copy, n_j) stages (rest zero).
+cudaError_t launch_head_gather(const std::int8_t* llr, const std::int64_t* blk_stage, int nblocks, int b, int v1,
+                               std::int64_t pitch, std::int64_t copy, std::int8_t* head, cudaStream_t stream);
 
 /// Device depuncture of stages [t0, t0 + n) (reference decoder.cpp:131-163):
 /// out[(t - t0) * b + row] = mask(row, t % period) ? next punctured byte : 0.

@@ -116,3 +116,31 @@ def test_batch_errors():
         vd.framed_decode_batch([np.zeros(10, np.int8), np.zeros(0, np.int8)], t, vd.FrameConfig(4))
     with pytest.raises(ValueError, match="at least one block"):
         vd.framed_decode_batch([], t, vd.FrameConfig(4))
+
+
+@pytest.mark.parametrize("code", [K7, (7, 3, [0o133, 0o171, 0o165]), (9, 2, [0o561, 0o753])],
+                         ids=lambda c: f"K{c[0]}B{c[1]}")
+def test_batch_head_and_tail_classes(code, port):
+    """Many blocks (the BER-sweep shape) so the fast kernel takes the block
+    heads (zero-padded head copies) and the clipped-v2 tails (one launch per
+    distinct v2'); block lengths chosen to give several tail classes."""
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng(77 + k + b)
+    for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(128, 24, 40), vd.FrameConfig(256, 20, 20, 0,
+                                                                                          vd.TracebackStart.kRandom, 3),
+                vd.FrameConfig(160, 20, 48, 32)):
+        lens = [int(x) for x in rng.choice([8192, 8192 + 4, 8192 + 12, 8192 + 36, 4096 + 8, 6000], size=300)]
+        blocks, exp = [], []
+        for j, n in enumerate(lens):
+            rx, _ = port.gen_bench_block(k, b, polys, n, 2.5, 50_000 + j)
+            q = oracle.quantize(rx, 32.0)
+            blocks.append(q)
+        got = vd.framed_decode_batch(blocks, t, cfg)
+        for j, n in enumerate(lens[:120]):  # oracle on a subset of blocks (time)
+            eb, est, _ = port.framed_decode(k, b, polys, blocks[j], n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start),
+                                            cfg.seed)
+            bits, st = got[j]
+            bad = np.flatnonzero(bits != eb)
+            assert bad.size == 0, (code, cfg, n, bad[:10])
+            assert (st.frames, st.stages, st.tracebacks) == est
