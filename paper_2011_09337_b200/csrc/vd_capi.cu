@@ -392,8 +392,8 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
     if (fast && (bstage[j] * B) % 4 == 0) {
       lo = (v1 + f - 1) / f;                                        // m*f >= v1
       hi = lens[j] - f - v2 >= 0 ? (lens[j] - f - v2) / f + 1 : 0;  // m*f + f + v2 <= n_j
-      // window + 4 stages of prefetch slack inside the whole stream
-      const std::int64_t room = n_total - bstage[j] + v1 - L - 4;
+      // window + the fast kernel's read slack inside the whole stream
+      const std::int64_t room = n_total - bstage[j] + v1 - L - vd::kPfSlackStages;
       hi = std::min(hi, room >= 0 ? room / f + 1 : 0);
       hi = std::max(hi, lo);
     }
@@ -409,7 +409,7 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
       if ((edge_mode & 1) && aligned && m < head_end && m * f + f + v2 <= lens[j]) {
         heads.push_back(bframe[j] + m);
       } else if ((edge_mode & 2) && aligned && one_tb && m >= head_end && m * f + f <= lens[j] && m * f + f + v2 > lens[j] &&
-                 f + v1 + (lens[j] - m * f - f) >= 16) {
+                 f + v1 + (lens[j] - m * f - f) >= 16 && bstage[j] + lens[j] + vd::kPfSlackStages <= n_total) {
         tails[static_cast<int>(lens[j] - m * f - f)].push_back(bframe[j] + m);
       } else {
         edges.push_back(bframe[j] + m);
@@ -487,7 +487,8 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
   std::vector<std::int64_t> back_to_generic;
   if constexpr (sizeof(T) == 1) {
     if (e == cudaSuccess && fast_launched && !heads.empty()) {
-      const std::int64_t pitch = (v1 + head_end * f + v2 + 3) & ~std::int64_t(3);  // 4-byte aligned block heads
+      // 4-byte aligned block heads, each followed by the fast kernel's read slack
+      const std::int64_t pitch = (v1 + head_end * f + v2 + vd::kPfSlackStages + 3) & ~std::int64_t(3);
       e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), static_cast<std::size_t>(pitch) * B * nblocks + 16, s);
       if (e == cudaSuccess)
         e = vd::launch_head_gather(reinterpret_cast<const std::int8_t*>(llr), p.blk_stage, nblocks, B, v1, pitch,

@@ -306,6 +306,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_RENORM_TABLE
 #define VD_RENORM_TABLE 1
 #endif
+#ifndef VD_PF_SLACK
+#define VD_PF_SLACK 1
+#endif
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2
 #endif
@@ -480,7 +483,11 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   // so two full blocks of work cover the HBM latency.
   // pf_room = words left in the frame window from pf: near the window end the
   // prefetch is clamped so it never reads past the LLRs the caller provided.
-  if (pf_room >= WPB) {
+  if (VD_PF_SLACK || pf_room >= WPB) {
+    // VD_PF_SLACK: every launched window is followed by >= 2 blocks of
+    // readable stages (plan() / the head copies / the batch tables guarantee
+    // it), so the prefetch never needs clamping; the over-read values are
+    // never consumed past stage L-1.
 #pragma unroll
     for (int i = 0; i < WPB; ++i) {
       st.llr[BUF][0][i] = ldg_pinned(pfA + i);
@@ -648,7 +655,7 @@ __global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
     return Slot{r.base + r.m * p.f - p.v1, r.m, r.blk, fp.llr_head != nullptr && r.m * p.f < p.v1};
   };
   const Slot slA = frame_slot(mA, validA), slB = frame_slot(mB, validB);
-  const std::int64_t wsA = slA.ws, wsB = slB.ws;
+
 
   const int f = static_cast<int>(opaque(static_cast<std::uint32_t>(p.f)));
   const int v1 = static_cast<int>(opaque(static_cast<std::uint32_t>(p.v1)));
@@ -1227,7 +1234,10 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
     fp.safe_stage = p.safe_stage;
     if (p.sigma) return false;
   } else {
-  const std::int64_t span = static_cast<std::int64_t>(fp.L) + 4;  // stages read per frame (word granularity slack)
+  // stages read per frame: the window rounded up to whole blocks, plus the
+  // two-block prefetch overrun when VD_PF_SLACK (else 4 stages of word slack)
+  const std::int64_t span = VD_PF_SLACK ? static_cast<std::int64_t>(fp.nblk) * GEO::LB + 2 * GEO::LB
+                                        : static_cast<std::int64_t>(fp.L) + 4;
   std::int64_t lo = pad_head ? p.frame_begin : (p.v1 + p.f - 1) / p.f;  // first m with m*f >= v1 (or padded head)
   std::int64_t hi_excl = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // m*f + f + v2 <= n
   // the caller guarantees LLRs up to the window end of the last launched frame
@@ -1352,7 +1362,8 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
     const std::int64_t stages = head_end * p.f + p.v2;  // window end of the last head frame (<= n: mi1 >= head_end)
     if (cudaError_t e = scratch_pool(); e != cudaSuccess) return e;
     // (+16 bytes: the last LLR word of a window may extend past the window's last stage)
-    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), (p.v1 + stages) * B + 16, stream);
+    if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), (p.v1 + stages + kPfSlackStages) * B + 16,
+                                        stream);
         e != cudaSuccess)
       return e;
     if (cudaError_t e = cudaMemsetAsync(head_buf, 0, static_cast<std::size_t>(p.v1) * B, stream); e != cudaSuccess)

@@ -76,6 +76,11 @@ __device__ __forceinline__ FrameRef resolve_frame(const DecodeLaunch& p, std::in
 cudaError_t launch_generic_i8(const DecodeLaunch& p, cudaStream_t stream);
 cudaError_t launch_generic_f64(const DecodeLaunch& p, cudaStream_t stream);
 
+/// Stages a fast-kernel window may read past its end (rounding to 4-stage
+/// blocks + the two-block LLR prefetch); callers building padded copies or
+/// choosing which frames go to the fast kernel keep this much readable slack.
+constexpr int kPfSlackStages = 12;
+
 /// Register-resident fast kernel. Returns cudaErrorNotSupported when the
 /// code/config is outside its envelope (caller then uses the generic one).
 bool fast_path_supported(const DecodeLaunch& p);
