@@ -218,13 +218,24 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # Plumbing test hook: VITDEC_BENCH_ONE_DEVICE=1 puts every rank on cuda:0
+    # with the gloo backend (NCCL refuses two ranks on one GPU), so the N > 1
+    # path (barriers, max-over-ranks timing, rank-0 reporting) can be exercised
+    # on a one-GPU box. Numbers from such a run are not scaling measurements.
+    one_dev = os.environ.get("VITDEC_BENCH_ONE_DEVICE") == "1"
+    if one_dev:
+        local = 0
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_dev:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
+    red_dev = torch.device("cpu") if one_dev else dev  # gloo reduces CPU tensors
 
     t = vd.build_trellis(vd.CodeSpec(*args.code))
     B = args.code[1]
@@ -266,7 +277,7 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1)
     if dist:
-        tt = torch.tensor([ms], device=dev)
+        tt = torch.tensor([ms], device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         ms = float(tt.item())
         dist.barrier()
@@ -298,7 +309,7 @@ def run_ours(args):
         e2e_step()
     e2e_s = (time.perf_counter() - t0) / e2e_reps
     if dist:
-        tt = torch.tensor([e2e_s], device=dev)
+        tt = torch.tensor([e2e_s], device=red_dev)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_s = float(tt.item())
     e2e_gbps = ne * world / e2e_s / 1e9
