@@ -3,12 +3,16 @@
 // trellis.cpp and decoder.cpp in a link: the decode entry points call the
 // GPU, everything else keeps the reference's semantics and exception
 // messages.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
 #include <string>
+#include <thread>
+#include <vector>
 
 #include "vitdec/decoder.hpp"
 #include "vitdec/trellis.hpp"
@@ -62,21 +66,51 @@ int env_gpus() {
 // True when every value is an integer in [-127, 127]: the block is then
 // decoded by the int8 fixed-point kernels, exactly (integer sums are exact in
 // both the reference's double arithmetic and the kernel's int32 arithmetic).
-bool int8_exact(const LlrBlock& llr, std::vector<std::int8_t>* q) {
+// Runs fn(lo, hi) over [0, n) on `workers` host threads (the reference's
+// `workers` argument, parallel.hpp:11-29 semantics: contiguous chunks, joined
+// before return); small ranges stay on the calling thread.
+template <typename Fn>
+void host_parallel(std::int64_t n, int workers, Fn&& fn) {
+  const std::int64_t w = std::max<std::int64_t>(1, std::min<std::int64_t>(workers, n / (1 << 20) + 1));
+  if (w <= 1) {
+    fn(std::int64_t{0}, n);
+    return;
+  }
+  const std::int64_t chunk = (n + w - 1) / w;
+  std::vector<std::thread> th;
+  for (std::int64_t i = 0; i < w; ++i) {
+    const std::int64_t lo = i * chunk, hi = std::min(n, lo + chunk);
+    if (lo >= hi) break;
+    th.emplace_back([&fn, lo, hi] { fn(lo, hi); });
+  }
+  for (auto& t : th) t.join();
+}
+
+// Integer-valued blocks in [-127, 127] decode exactly on the int8 kernels.
+bool int8_exact(const LlrBlock& llr, std::vector<std::int8_t>* q, int workers) {
   const Eigen::Index n = llr.size();
   q->resize(static_cast<std::size_t>(n));
   const double* d = llr.data();
-  for (Eigen::Index i = 0; i < n; ++i) {
-    const double v = d[i];
-    if (!(v >= -127.0 && v <= 127.0) || std::nearbyint(v) != v) return false;
-    (*q)[static_cast<std::size_t>(i)] = static_cast<std::int8_t>(v);
-  }
-  return true;
+  std::int8_t* out = q->data();
+  std::atomic<bool> ok{true};
+  host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
+    bool good = true;
+    for (std::int64_t i = lo; i < hi; ++i) {  // branch-free body: vectorisable
+      const double v = d[i];
+      const double r = std::nearbyint(v);
+      good &= (v >= -127.0) & (v <= 127.0) & (r == v);
+      out[i] = static_cast<std::int8_t>(good ? r : 0.0);
+    }
+    if (!good) ok.store(false, std::memory_order_relaxed);
+  });
+  return ok.load();
 }
 
-BitVec unpack(const std::vector<std::uint32_t>& packed, Eigen::Index n) {
+BitVec unpack(const std::vector<std::uint32_t>& packed, Eigen::Index n, int workers = 1) {
   BitVec bits(static_cast<std::size_t>(n));
-  for (Eigen::Index i = 0; i < n; ++i) bits[i] = static_cast<std::uint8_t>((packed[i >> 5] >> (i & 31)) & 1u);
+  host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
+    for (std::int64_t i = lo; i < hi; ++i) bits[i] = static_cast<std::uint8_t>((packed[i >> 5] >> (i & 31)) & 1u);
+  });
   return bits;
 }
 
@@ -211,7 +245,7 @@ LlrBlock depuncture(const Eigen::Ref<const Eigen::ArrayXd>& punctured, const Pun
 
 // ---- decoder.hpp: GPU decode entry points ---------------------------------
 
-DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const FrameConfig& cfg, int /*workers*/) {
+DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const FrameConfig& cfg, int workers) {
   check_block(llr, trellis);
   cfg.validate();
   const vd_frame_cfg c = to_c(cfg);
@@ -221,13 +255,14 @@ DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const Fr
   vd_exec ex{};
   ex.num_devices = env_gpus();
   std::vector<std::int8_t> q;
-  if (int8_exact(llr, &q)) {
+  // `workers` host threads prepare the block / unpack the bits (the GPU does the decode)
+  if (int8_exact(llr, &q, workers)) {
     check(vd_decode_i8(trellis.native(), &c, q.data(), n, packed.data(), &st, &ex));
   } else {
     check(vd_decode_f64(trellis.native(), &c, llr.data(), n, packed.data(), &st, &ex));
   }
   DecodeOutput out;
-  out.bits = unpack(packed, n);
+  out.bits = unpack(packed, n, workers);
   out.stats = from_c(st);
   return out;
 }
@@ -238,7 +273,7 @@ DecodeOutput serial_decode(const LlrBlock& llr, const Trellis& trellis) {
   std::vector<std::uint32_t> packed(static_cast<std::size_t>((n + 31) / 32));
   vd_stats st{};
   std::vector<std::int8_t> q;
-  if (n <= 0x7fffffff && int8_exact(llr, &q)) {
+  if (n <= 0x7fffffff && int8_exact(llr, &q, 1)) {
     // One frame covering the block with no overlap == serial_decode
     // (reference acceptance.cpp:57-81 equivalence).
     vd_frame_cfg c{};

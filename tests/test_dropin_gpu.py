@@ -25,3 +25,16 @@ def test_reference_unit_suite_on_gpu_decoder():
     print(r.stderr[-4000:])
     assert r.returncode == 0, r.stderr[-4000:]
     assert "Status: SUCCESS!" in r.stdout
+
+
+WORKERS_BIN = ROOT / "oracle" / "_ref" / "dropin_workers"
+
+
+@pytest.mark.skipif(not WORKERS_BIN.exists(), reason="drop-in workers check not built (make -C oracle dropin)")
+def test_dropin_api_workers_and_native_overload():
+    """tests/cpp/dropin_workers.cpp: vitdec::framed_decode(LlrBlock, ..., workers)
+    with 1 and 8 host threads and the native int8 overload agree bit for bit
+    on a 3 Mi-stage block; real-valued blocks (FP64 kernel) too."""
+    r = subprocess.run([str(WORKERS_BIN)], capture_output=True, text=True, timeout=600, cwd="/tmp")
+    print(r.stdout[-2000:], r.stderr[-2000:])
+    assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
