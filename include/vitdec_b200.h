@@ -207,6 +207,21 @@ vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg*
                                         const int8_t* punctured_dev, int64_t n_punctured, int8_t* llr_scratch_dev,
                                         uint32_t* out_dev, vd_stats* stats, int32_t device, void* stream);
 
+/* ---- 4-bit LLR wire format --------------------------------
+ * Two signed 4-bit LLRs per byte, element i of the stage-major stream (t*B + b)
+ * in nibble i (low nibble first), values in [-8, 7] (e.g. the quantiser
+ * clamp(rint(scale * y), -7, 7)). Decoding is exact for those integer LLRs:
+ * identical to vd_decode_i8 on the same values widened to int8. */
+
+/* framed_decode on a 4-bit host stream: only the packed bytes cross PCIe
+ * (1 byte per r1/2 stage), each chunk is widened on the device. Same output,
+ * stats, sharding and threading as vd_decode_i8. */
+vd_status vd_decode_i4(const vd_code* code, const vd_frame_cfg* cfg, const uint8_t* llr4, int64_t n_stages,
+                       uint32_t* out_packed, vd_stats* stats, const vd_exec* exec);
+/* Widen `count` 4-bit LLRs (device, 4-byte aligned) to int8 (device, 8-byte
+ * aligned). Asynchronous. */
+vd_status vd_unpack_i4_device(const uint8_t* llr4_dev, int64_t count, int8_t* llr_dev, int32_t device, void* stream);
+
 /* serial_decode (reference decoder.cpp:101-129): one frame, no overlap. */
 vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n_stages, uint32_t* out_packed,
                                vd_stats* stats, int32_t device);

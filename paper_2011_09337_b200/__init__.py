@@ -22,10 +22,13 @@ from .api import (
     framed_decode_batch,
     framed_decode_punctured,
     framed_decode_stream,
+    framed_decode_stream_i4,
     pack_bits,
+    pack_i4,
     partition_frames,
     serial_decode,
     unpack_bits,
+    unpack_i4,
 )
 
 __all__ = [
@@ -47,8 +50,11 @@ __all__ = [
     "framed_decode_batch",
     "framed_decode_punctured",
     "framed_decode_stream",
+    "framed_decode_stream_i4",
     "pack_bits",
+    "pack_i4",
     "partition_frames",
     "serial_decode",
     "unpack_bits",
+    "unpack_i4",
 ]

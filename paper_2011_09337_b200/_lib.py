@@ -80,6 +80,8 @@ SIGNATURES = {
                                      C.POINTER(VdExec)]),
     "vd_decode_punctured_i8_device": (I32, [P, C.POINTER(VdFrameCfg), C.POINTER(VdPuncture), P, I64, P, P,
                                             C.POINTER(VdStats), I32, P]),
+    "vd_decode_i4": (I32, [P, C.POINTER(VdFrameCfg), P, I64, P, C.POINTER(VdStats), C.POINTER(VdExec)]),
+    "vd_unpack_i4_device": (I32, [P, I64, P, I32, P]),
     "vd_last_error": (C.c_char_p, []),
     "vd_version": (C.c_char_p, []),
 }

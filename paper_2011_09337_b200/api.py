@@ -423,3 +423,43 @@ def framed_decode_punctured(punctured: np.ndarray, pattern: PuncturePattern, tre
     check(lib().vd_decode_punctured_i8(trellis.handle, C.byref(c), C.byref(pc), arr.ctypes.data, arr.size,
                                        out.ctypes.data, C.byref(st), C.byref(ex)))
     return out, n, _stats(st)
+
+
+# ---- 4-bit LLR wire format -----------------------------------
+
+
+def pack_i4(llr: np.ndarray) -> np.ndarray:
+    """int8 LLRs in [-8, 7] (stage-major) -> 4-bit wire format: element i in
+    nibble i, low nibble first (include/vitdec_b200.h)."""
+    a = np.ascontiguousarray(llr, dtype=np.int8).reshape(-1)
+    if a.size and (a.min() < -8 or a.max() > 7):
+        raise ValueError("4-bit LLRs must lie in [-8, 7]")
+    nib = (a.astype(np.int16) & 0xF).astype(np.uint8)
+    if nib.size % 2:
+        nib = np.concatenate([nib, np.zeros(1, np.uint8)])
+    return (nib[0::2] | (nib[1::2] << 4)).astype(np.uint8)
+
+
+def unpack_i4(packed: np.ndarray, count: int) -> np.ndarray:
+    """Inverse of pack_i4 (host reference for the device unpack)."""
+    p = np.ascontiguousarray(packed, dtype=np.uint8)
+    nib = np.empty(p.size * 2, np.uint8)
+    nib[0::2] = p & 0xF
+    nib[1::2] = p >> 4
+    v = nib[:count].astype(np.int8)
+    return np.where(v >= 8, v - 16, v).astype(np.int8)
+
+
+def framed_decode_stream_i4(llr4: np.ndarray, n: int, trellis: Trellis, cfg: FrameConfig, gpus: int = 0,
+                            chunk_stages: int = 0):
+    """framed_decode on a 4-bit wire-format stream (vd_decode_i4) -> (packed bits, DecodeStats)."""
+    arr = np.ascontiguousarray(llr4, dtype=np.uint8).reshape(-1)
+    if arr.size * 2 < n * trellis.outputs_per_bit():
+        raise ValueError("4-bit stream shorter than n * B values")
+    out = np.zeros((n + 31) // 32, np.uint32)
+    st = VdStats()
+    c = cfg.to_c()
+    ex = _exec(gpus, chunk_stages)
+    check(lib().vd_decode_i4(trellis.handle, C.byref(c), arr.ctypes.data, n, out.ctypes.data, C.byref(st),
+                             C.byref(ex)))
+    return out, _stats(st)

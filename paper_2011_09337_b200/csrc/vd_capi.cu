@@ -608,10 +608,13 @@ struct Chunk {
 // pp != nullptr (int8 only): `llr` is the PUNCTURED stream of pattern pp
 // covering n stages; each chunk's punctured bytes are copied and expanded on
 // the device (depuncture kernel) right before its decode.
+// llr4 != nullptr (int8 only): the stream is in the 4-bit wire format
+// (element i in nibble i of llr4, low nibble first); each chunk's bytes are
+// copied and widened to int8 on the device (vd_wire.cu) before its decode.
 template <typename T>
 vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr, std::int64_t n,
                       std::uint32_t* out_packed, vd_stats* stats, const vd_exec* exec,
-                      const PunctPlan* pp = nullptr) {
+                      const PunctPlan* pp = nullptr, const std::uint8_t* llr4 = nullptr) {
   if (!code) return fail(VD_EINVAL, "null code");
   if (n < 1) return fail(VD_EINVAL, "empty llr block");
   if (vd_status st = validate_cfg(cfg, 1)) return st;
@@ -670,7 +673,7 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
     for (int i = 0; i < 2; ++i) {
       if (!ctx.st[i]) VD_CUDA(cudaStreamCreateWithFlags(&ctx.st[i], cudaStreamNonBlocking), "cudaStreamCreate");
       if (vd_status st = ensure(&ctx.llr[i], &ctx.llr_cap[i], llr_bytes)) return st;
-      if (pp) {
+      if (pp || llr4) {
         if (vd_status st = ensure(&ctx.pun[i], &ctx.pun_cap[i], llr_bytes)) return st;
       }
       void* o = ctx.out[i];
@@ -699,6 +702,14 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
         if (vd_status st = launch_depuncture(*pp, static_cast<const std::int8_t*>(ctx.pun[slot]), wb, we - wb,
                                              reinterpret_cast<std::int8_t*>(dl), s))
           return st;
+      } else if (llr4) {
+        const std::int64_t e0 = wb * code->b, e1 = we * code->b;  // element range of the chunk
+        const std::int64_t by0 = e0 >> 1, by1 = (e1 + 1) >> 1;
+        VD_CUDA(cudaMemcpyAsync(ctx.pun[slot], llr4 + by0, by1 - by0, cudaMemcpyHostToDevice, s), "H2D i4 chunk");
+        const cudaError_t eu = vd::launch_unpack_i4(static_cast<const std::uint8_t*>(ctx.pun[slot]),
+                                                    static_cast<int>(e0 & 1), e1 - e0,
+                                                    reinterpret_cast<std::int8_t*>(dl), s);
+        if (eu != cudaSuccess) return cuda_fail(eu, "unpack i4 kernel");
       } else {
         VD_CUDA(cudaMemcpyAsync(dl, llr + wb * code->b, sizeof(T) * (we - wb) * code->b, cudaMemcpyHostToDevice, s),
                 "H2D llr chunk");
@@ -1004,6 +1015,26 @@ vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg*
   if (vd_status st = launch_depuncture(pp, punctured_dev, 0, n, llr_scratch_dev, s)) return st;
   return decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, 0, 0, num_frames(cfg, n), out_dev, 0, nullptr,
                                     dev, stream);
+}
+
+vd_status vd_decode_i4(const vd_code* code, const vd_frame_cfg* cfg, const uint8_t* llr4, int64_t n, uint32_t* out,
+                       vd_stats* stats, const vd_exec* exec) {
+  if (!llr4) return fail(VD_EINVAL, "null buffer");
+  return decode_host<std::int8_t>(code, cfg, reinterpret_cast<const std::int8_t*>(llr4), n, out, stats, exec, nullptr,
+                                  llr4);
+}
+
+vd_status vd_unpack_i4_device(const uint8_t* llr4_dev, int64_t count, int8_t* llr_dev, int32_t device, void* stream) {
+  if (count < 0) return fail(VD_EINVAL, "negative count");
+  if (count == 0) return VD_OK;
+  if (!llr4_dev || !llr_dev) return fail(VD_EINVAL, "null buffer");
+  int dev = 0;
+  if (vd_status st = resolve_device(device, &dev)) return st;
+  DeviceGuard guard(dev);
+  const cudaError_t e = vd::launch_unpack_i4(llr4_dev, 0, count, llr_dev, static_cast<cudaStream_t>(stream));
+  if (e == cudaErrorMisalignedAddress) return fail(VD_EINVAL, "llr4_dev must be 4-byte and llr_dev 8-byte aligned");
+  if (e != cudaSuccess) return cuda_fail(e, "unpack i4 kernel");
+  return VD_OK;
 }
 
 vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n, uint32_t* out, vd_stats* stats,

@@ -112,6 +112,11 @@ struct DepunctureLaunch {
 };
 cudaError_t launch_depuncture_i8(const DepunctureLaunch& p, cudaStream_t stream);
 
+/// 4-bit wire format: widen `count` signed nibbles (element i in nibble
+/// nib_off + i of `in`, low nibble first) to int8 at `out` (8-byte aligned).
+cudaError_t launch_unpack_i4(const std::uint8_t* in, int nib_off, std::int64_t count, std::int8_t* out,
+                             cudaStream_t stream);
+
 cudaError_t launch_synth_i8(int k, int b, const std::uint32_t* polys, std::int64_t n, double sigma, double scale,
                             std::uint64_t seed, std::int8_t* llr, std::uint32_t* bits, cudaStream_t stream);
 cudaError_t launch_count_bit_errors(const std::uint32_t* a, const std::uint32_t* b, std::int64_t n_bits,
