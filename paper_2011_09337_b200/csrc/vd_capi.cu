@@ -37,6 +37,10 @@ struct vd_code {
   }
 };
 
+#ifndef VD_SERIAL_PARALLEL
+#define VD_SERIAL_PARALLEL 1
+#endif
+
 namespace {
 
 thread_local std::string g_err;
@@ -287,6 +291,8 @@ vd_status decode_device(const vd_code* code, const vd_frame_cfg* cfg, std::int64
   if constexpr (sizeof(T) == 1) {
     if (vd::fast_path_supported(p)) {
       e = vd::launch_fast_i8(p, s);
+    } else if (VD_SERIAL_PARALLEL && vd::serial_parallel_supported(p)) {
+      e = vd::launch_serial_parallel_i8(p, s);
     } else {
       e = vd::launch_generic_i8(p, s);
     }

@@ -33,6 +33,7 @@ namespace {
 
 constexpr int kWarps = 4;     // warps (frames in flight) per CTA
 constexpr int kStage = 128;   // LLR staging depth (stages) per warp
+constexpr int kTbChunk = 512; // traceback staging chunk (stages) for decisions held in global memory
 constexpr unsigned kFull = 0xffffffffu;
 
 struct GenericParams {
@@ -44,6 +45,7 @@ struct GenericParams {
   std::uint32_t* dec_global;  // [total_warps][len_max * words] when !dec_in_smem
   int smem_per_warp;          // bytes
   int stage_off, dec_off;     // byte offsets inside a warp's area
+  int tb_off;                 // reg_kernel with global decisions: traceback staging (kTbChunk stages)
 };
 
 template <typename M>
@@ -223,14 +225,18 @@ __global__ void __launch_bounds__(kWarps * 32) generic_kernel(const GenericParam
 // shuffle -> add -> compare -> select (no shared-memory round trip or
 // __syncwarp between stages). Branch metrics are evaluated per lane straight
 // from the stage LLRs in the reference's add order (decoder.cpp:41-51).
-template <typename In, typename M, int NPL>
+// BT > 0: B known at compile time (2, 3, 4): the stage's 2^(B-1) direct
+// branch metrics are computed once per stage in the reference's add order
+// and each state edge picks its entry (+ sign) with a precomputed index
+// (BT = 0: any B, evaluated per edge).
+template <typename In, typename M, int NPL, int BT>
 __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp) {
   const DecodeLaunch& p = gp.p;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int lane = threadIdx.x & 31;
   const int warp = threadIdx.x >> 5;
   const int S = p.s;
-  const int b = p.b;
+  const int b = BT > 0 ? BT : p.b;
   const std::uint32_t half = 1u << (b - 1);
   const std::uint32_t tmask = (1u << b) - 1u;
 
@@ -274,6 +280,33 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
     }
     return neg ? -acc : acc;
   };
+  // compile-time-B form: per edge, direct-table index and complement flag
+  constexpr int NT = BT > 0 ? (1 << (BT - 1)) : 1;
+  std::uint32_t eidx[NPL][2];
+  bool eneg[NPL][2];
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      eneg[r][e] = lab[r][e] >= half;
+      eidx[r][e] = eneg[r][e] ? (lab[r][e] ^ tmask) : lab[r][e];
+    }
+  }
+  auto stage_table = [&](const M* v, M (&T)[NT]) {
+#pragma unroll
+    for (int x = 0; x < NT; ++x) {
+      M acc = M(0);  // reference decoder.cpp:22-30 order: 0 + (+/-v0) + (+/-v1) ...
+#pragma unroll
+      for (int i = 0; i < (BT > 0 ? BT : 1); ++i) acc += ((x >> ((BT > 0 ? BT : 1) - 1 - i)) & 1) ? -v[i] : v[i];
+      T[x] = acc;
+    }
+  };
+  auto pick = [&](const M (&T)[NT], std::uint32_t idx, bool neg) -> M {
+    M val = T[0];
+#pragma unroll
+    for (int x = 1; x < NT; ++x) val = idx == static_cast<std::uint32_t>(x) ? T[x] : val;
+    return neg ? -val : val;
+  };
 
   for (std::int64_t mi = p.frame_begin + gwarp; mi < p.frame_end; mi += total_warps) {
     const FrameRef fr = resolve_frame(p, mi);
@@ -284,14 +317,15 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
 #pragma unroll
     for (int r = 0; r < NPL; ++r) sig[r] = M(0);  // sigma_0 = 0 (decoder.cpp:195)
     std::int64_t offset = 0;
-    std::int64_t next_record = 0;
-    std::int64_t next_start = g.start_stage(0, p.v2);
+    int next_record = 0;
+    int next_start = static_cast<int>(g.start_stage(0, p.v2));
     const In* src = llr + (fr.base + g.beg - p.llr_stage0) * b;
+    const int len32 = static_cast<int>(len);  // frame windows < 2^31 stages (checked at launch)
 
-    auto refill = [&](std::int64_t t) {
-      const std::int64_t cnt = imin(kStage, len - t) * b;
+    auto refill = [&](int t) {
+      const int cnt = (kStage < len32 - t ? kStage : len32 - t) * b;
       __syncwarp();
-      for (std::int64_t i = lane; i < cnt; i += 32) stage_buf[i] = src[t * b + i];
+      for (int i = lane; i < cnt; i += 32) stage_buf[i] = src[static_cast<std::int64_t>(t) * b + i];
       __syncwarp();
     };
     M v[8];
@@ -300,14 +334,24 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
 #pragma unroll
       for (int i = 0; i < 8; ++i) v[i] = i < b ? static_cast<M>(stage_buf[i]) : M(0);
     }
-    for (std::int64_t t = 0; t < len; ++t) {
+    for (int t = 0; t < len32; ++t) {
       M bmv[NPL][2];
+      if constexpr (BT > 0) {
+        M T[NT];
+        stage_table(v, T);
 #pragma unroll
-      for (int r = 0; r < NPL; ++r) {
-        bmv[r][0] = bm(v, lab[r][0]);
-        bmv[r][1] = bm(v, lab[r][1]);
+        for (int r = 0; r < NPL; ++r) {
+          bmv[r][0] = pick(T, eidx[r][0], eneg[r][0]);
+          bmv[r][1] = pick(T, eidx[r][1], eneg[r][1]);
+        }
+      } else {
+#pragma unroll
+        for (int r = 0; r < NPL; ++r) {
+          bmv[r][0] = bm(v, lab[r][0]);
+          bmv[r][1] = bm(v, lab[r][1]);
+        }
       }
-      if (t + 1 < len) {  // software pipeline: next stage's LLRs
+      if (t + 1 < len32) {  // software pipeline: next stage's LLRs
         if (((t + 1) & (kStage - 1)) == 0) refill(t + 1);
         const In* lt = stage_buf + ((t + 1) & (kStage - 1)) * b;
 #pragma unroll
@@ -379,7 +423,7 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
         }
         if (lane == 0) start_state[next_record] = bi;
         ++next_record;
-        if (next_record < g.num_sub) next_start = g.start_stage(next_record, p.v2);
+        if (next_record < g.num_sub) next_start = static_cast<int>(g.start_stage(next_record, p.v2));
       }
     }
     __syncwarp();
@@ -401,7 +445,65 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
     // The decision words of 4 stages are loaded before the state chain walks
     // them, so the chain is select + shift instead of a load per stage.
     const std::uint32_t lmask = static_cast<std::uint32_t>(S / 2 - 1);
-    for (std::int64_t s = lane; s < g.num_sub; s += 32) {
+    if (g.num_sub == 1) {
+      // One traceback per frame (f0 == 0, serial_decode): lane 0 walks from
+      // the stored-max state with the decision words of 8 stages loaded ahead
+      // (they do not depend on the traced path), so the state chain is pure
+      // ALU; emitted bits gather in a 32-bit word flushed every 32 stages.
+      // Decisions held in global memory (long frames) are first staged into
+      // shared memory in chunks of kTbChunk stages with coalesced loads.
+      std::uint32_t* tb = reinterpret_cast<std::uint32_t*>(base + gp.tb_off);
+      const int st = static_cast<int>(g.start_stage(0, p.v2));
+      const int tend = static_cast<int>(g.sub_lo(0) - g.beg);
+      const int temit = static_cast<int>(g.sub_hi(0) - g.beg);  // stages t < temit emit a bit
+      const std::int64_t rel0 = fr.base + g.beg - p.out_stage0;  // output bit of stage t = 0
+      const std::uint32_t rlo = static_cast<std::uint32_t>(rel0);
+      const int ksh = p.k - 2;
+      std::uint32_t state = static_cast<std::uint32_t>(start_state[0]);  // num_sub == 1: stored max
+      std::uint32_t acc = 0;
+      auto step = [&](int t, std::uint32_t word) {
+        if (t < temit) {
+          const std::uint32_t pos = (rlo + static_cast<std::uint32_t>(t)) & 31u;
+          acc |= (state >> ksh) << pos;
+          if (pos == 0 || t == tend) {
+            if (acc) atomicOr(p.out + ((rel0 + t) >> 5), acc);
+            acc = 0;
+          }
+        }
+        state = ((state & lmask) << 1) | ((word >> (state & 31)) & 1u);
+      };
+      for (int chi = st; chi >= tend; chi -= kTbChunk) {
+        const int clo = chi - kTbChunk + 1 > tend ? chi - kTbChunk + 1 : tend;
+        const std::uint32_t* src = dec;
+        if (!gp.dec_in_smem) {
+          const int cnt = (chi - clo + 1) * NPL;
+          __syncwarp();
+          for (int i = lane; i < cnt; i += 32) tb[i] = dec[clo * NPL + i];
+          __syncwarp();
+          src = tb - clo * NPL;
+        }
+        if (lane == 0) {
+          int t = chi;
+          for (; t - 7 >= clo; t -= 8) {
+            std::uint32_t wv[8][NPL];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+#pragma unroll
+              for (int r = 0; r < NPL; ++r) wv[u][r] = src[(t - u) * NPL + r];
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+              std::uint32_t word = wv[u][0];
+#pragma unroll
+              for (int r = 1; r < NPL; ++r) word = (state >> 5) == static_cast<std::uint32_t>(r) ? wv[u][r] : word;
+              step(t - u, word);
+            }
+          }
+          for (; t >= clo; --t) step(t, src[t * NPL + (NPL > 1 ? (state >> 5) : 0)]);
+        }
+      }
+    }
+    for (std::int64_t s = lane; s < g.num_sub && g.num_sub > 1; s += 32) {
       const std::int64_t st = g.start_stage(s, p.v2);
       const std::int64_t lo = g.sub_lo(s), hi = g.sub_hi(s);
       std::uint32_t state;
@@ -452,7 +554,7 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
   }
 }
 
-template <typename In, typename M, int NPL>
+template <typename In, typename M, int NPL, int BT>
 cudaError_t launch_reg(GenericParams gp, cudaStream_t stream) {
   const DecodeLaunch& p = gp.p;
   const std::int64_t frames = p.frame_end - p.frame_begin;
@@ -463,7 +565,10 @@ cudaError_t launch_reg(GenericParams gp, cudaStream_t stream) {
   const std::size_t dec_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>(gp.len_max) * NPL;
   constexpr std::size_t kSmemBudget = 200 * 1024;
   gp.dec_in_smem = (head + stage_bytes + dec_bytes) * kWarps <= kSmemBudget;
-  const std::size_t per_warp = ((gp.dec_in_smem ? head + stage_bytes + dec_bytes : head + stage_bytes) + 15) & ~std::size_t(15);
+  const std::size_t tb_bytes = sizeof(std::uint32_t) * kTbChunk * NPL;
+  gp.tb_off = static_cast<int>(head + stage_bytes);
+  const std::size_t per_warp =
+      ((gp.dec_in_smem ? head + stage_bytes + dec_bytes : head + stage_bytes + tb_bytes) + 15) & ~std::size_t(15);
   if (per_warp * kWarps > kSmemBudget) return cudaErrorInvalidValue;
   gp.smem_per_warp = static_cast<int>(per_warp);
   std::int64_t blocks = (frames + kWarps - 1) / kWarps;
@@ -476,7 +581,7 @@ cudaError_t launch_reg(GenericParams gp, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
   }
   const std::size_t smem = per_warp * kWarps;
-  auto kern = reg_kernel<In, M, NPL>;
+  auto kern = reg_kernel<In, M, NPL, BT>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e == cudaSuccess) {
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(gp);
@@ -505,11 +610,20 @@ cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
   if (frames <= 0) return cudaSuccess;
 
   if (p.s <= 256) {
-    switch (p.s <= 32 ? 1 : p.s / 32) {
-      case 1: return launch_reg<In, M, 1>(gp, stream);
-      case 2: return launch_reg<In, M, 2>(gp, stream);
-      case 4: return launch_reg<In, M, 4>(gp, stream);
-      case 8: return launch_reg<In, M, 8>(gp, stream);
+    const int npl = p.s <= 32 ? 1 : p.s / 32;
+    auto by_b = [&](auto npl_tag) -> cudaError_t {
+      constexpr int NPLc = decltype(npl_tag)::value;
+      switch (p.b) {
+        case 2: return launch_reg<In, M, NPLc, 2>(gp, stream);
+        case 3: return launch_reg<In, M, NPLc, 3>(gp, stream);
+        default: return launch_reg<In, M, NPLc, 0>(gp, stream);
+      }
+    };
+    switch (npl) {
+      case 1: return by_b(std::integral_constant<int, 1>{});
+      case 2: return by_b(std::integral_constant<int, 2>{});
+      case 4: return by_b(std::integral_constant<int, 4>{});
+      case 8: return by_b(std::integral_constant<int, 8>{});
       default: break;
     }
   }

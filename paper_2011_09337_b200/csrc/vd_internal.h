@@ -85,6 +85,11 @@ constexpr int kPfSlackStages = 12;
 /// code/config is outside its envelope (caller then uses the generic one).
 bool fast_path_supported(const DecodeLaunch& p);
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream);
+/// Exact segment-parallel decode of one long frame (serial_decode, f >= N;
+/// max-plus transfer matrices, vd_serial.cu). S <= 64, B in {2, 3}, int8.
+bool serial_parallel_supported(const DecodeLaunch& p);
+cudaError_t launch_serial_parallel_i8(const DecodeLaunch& p, cudaStream_t stream);
+
 /// Zero-padded block heads for the fast kernel: for every block j of the
 /// batch (blk_stage: device [nblocks + 1]), head[j * pitch * b ...] = v1 zero
 /// stages followed by the block's first min(copy, n_j) stages (rest zero).

@@ -1,0 +1,372 @@
+// Exact parallel decode of ONE long frame (reference serial_decode,
+// decoder.cpp:101-129, and framed_decode frames with f >= N): the forward
+// recursion sigma_t = A_t (x) sigma_{t-1} is a max-plus matrix-vector
+// product, and max-plus products are associative and exact on integers, so
+// the stage chain is cut into segments:
+//
+//   A  segment_matrix_kernel  per segment g and start state j (one warp each):
+//      the forward pass from the unit vector e_j (0 at j, -inf elsewhere)
+//      gives column j of the segment transfer matrix M_g (M_g[i][j] = best
+//      metric of a path j -> i through the segment). No decisions.
+//   B  boundary_kernel        one warp, sequential over segments:
+//      sigma_{g+1} = M_g (x) sigma_g (64 x 64 max-plus mat-vec, int64).
+//   C  segment_forward_kernel per segment (one warp each): the ordinary
+//      forward pass from the exact sigma_g, storing the decision words; the
+//      last segment also takes the argmax of the final metrics (lowest state
+//      on ties, decoder.cpp:80-90).
+//   D1 segment_map_kernel     per segment: trace back from every end state
+//      through the segment (one chain per state) -> map_g[state].
+//   D2 chain_kernel           one thread: end state of every segment by
+//      composing the maps from the final argmax.
+//   D3 segment_emit_kernel    per segment: trace back from its end state and
+//      write its decoded bits.
+//
+// Decisions are computed from the same integer metrics up to a per-segment
+// common offset, so every decision (ties included, decoder.cpp:67-74) and the
+// decoded bits are identical to the sequential decode. int8 LLRs only (double
+// sums are not associative).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <climits>
+#include <cstdint>
+
+#include "vd_common.cuh"
+#include "vd_internal.h"
+
+namespace vd {
+namespace {
+
+constexpr unsigned kFull = 0xffffffffu;
+constexpr std::int32_t kNeg = -(1 << 28);  // "-inf" for the unit start vectors
+
+struct SerialParams {
+  const std::int8_t* llr;  // stage beg of the frame window
+  int k, b, s;
+  std::int64_t len;        // window stages
+  int seg_len, nseg;
+  const std::uint32_t* in_out;
+  std::int32_t* mat;       // [nseg][S (j)][S (i)]: column-major per segment
+  std::int64_t* sig0;      // [nseg + 1][S]: metrics before each segment
+  std::uint32_t* dec;      // [len][NPL] decision words
+  std::int32_t* map;       // [nseg][S]
+  std::int32_t* endst;     // [nseg]: traced state at each segment's last stage; endst[nseg] = final argmax
+  std::uint32_t* out;      // packed output, bit of window stage t at out_bit0 + t
+  std::int64_t out_bit0;
+  std::int64_t emit_lo, emit_hi;  // window stages whose bits are written
+};
+
+template <int NPL, int BT>
+struct Lane {
+  std::uint32_t eidx[NPL][2];
+  bool eneg[NPL][2];
+  int srcA, srcB;
+  bool upper;
+  __device__ void init(const SerialParams& p, int lane) {
+    const std::uint32_t half = 1u << (BT - 1), tmask = (1u << BT) - 1u;
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) {
+      const int j = r * 32 + lane;
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const std::uint32_t x = j < p.s ? __ldg(p.in_out + 2 * j + e) : 0u;
+        eneg[r][e] = x >= half;
+        eidx[r][e] = eneg[r][e] ? (x ^ tmask) : x;
+      }
+    }
+    const int low = p.s / 2 - 1;
+    srcA = NPL == 1 ? (((lane & low) << 1) & 31) : ((2 * lane) & 31);
+    srcB = NPL == 1 ? ((((lane & low) << 1) | 1) & 31) : ((2 * lane + 1) & 31);
+    upper = lane >= 16;
+  }
+  // one ACS stage (reference decoder.cpp:53-76); returns the decision bits
+  __device__ __forceinline__ void stage(const std::int8_t* l, std::int32_t (&sig)[NPL], bool (&d)[NPL]) const {
+    constexpr int NT = 1 << (BT - 1);
+    std::int32_t v[BT];
+#pragma unroll
+    for (int i = 0; i < BT; ++i) v[i] = l[i];
+    std::int32_t T[NT];
+#pragma unroll
+    for (int x = 0; x < NT; ++x) {
+      std::int32_t acc = 0;
+#pragma unroll
+      for (int i = 0; i < BT; ++i) acc += ((x >> (BT - 1 - i)) & 1) ? -v[i] : v[i];
+      T[x] = acc;
+    }
+    auto pick = [&](std::uint32_t idx, bool neg) {
+      std::int32_t val = T[0];
+#pragma unroll
+      for (int x = 1; x < NT; ++x) val = idx == static_cast<std::uint32_t>(x) ? T[x] : val;
+      return neg ? -val : val;
+    };
+    std::int32_t ns[NPL];
+#pragma unroll
+    for (int q = 0; q < (NPL == 1 ? 1 : NPL / 2); ++q) {
+      std::int32_t pa, pb;
+      if constexpr (NPL == 1) {
+        pa = __shfl_sync(kFull, sig[0], srcA);
+        pb = __shfl_sync(kFull, sig[0], srcB);
+      } else {
+        const std::int32_t a0 = __shfl_sync(kFull, sig[2 * q], srcA), a1 = __shfl_sync(kFull, sig[2 * q + 1], srcA);
+        const std::int32_t b0 = __shfl_sync(kFull, sig[2 * q], srcB), b1 = __shfl_sync(kFull, sig[2 * q + 1], srcB);
+        pa = upper ? a1 : a0;
+        pb = upper ? b1 : b0;
+      }
+#pragma unroll
+      for (int h = 0; h < (NPL == 1 ? 1 : 2); ++h) {
+        const int r = q + h * (NPL / 2);
+        const std::int32_t s1 = pa + pick(eidx[r][0], eneg[r][0]);
+        const std::int32_t s2 = pb + pick(eidx[r][1], eneg[r][1]);
+        d[r] = !(s1 > s2);  // ties -> second predecessor
+        ns[r] = d[r] ? s2 : s1;
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) sig[r] = ns[r];
+  }
+};
+
+template <int NPL, int BT>
+__global__ void __launch_bounds__(128) segment_matrix_kernel(const SerialParams p) {
+  const int lane = threadIdx.x & 31;
+  const std::int64_t wid = static_cast<std::int64_t>(blockIdx.x) * 4 + (threadIdx.x >> 5);
+  if (wid >= static_cast<std::int64_t>(p.nseg) * p.s) return;  // whole warps only
+  const int g = static_cast<int>(wid / p.s), j = static_cast<int>(wid % p.s);
+  Lane<NPL, BT> ln;
+  ln.init(p, lane);
+  std::int32_t sig[NPL];
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) sig[r] = (r * 32 + lane == j) ? 0 : kNeg;
+  const std::int64_t t0 = static_cast<std::int64_t>(g) * p.seg_len;
+  const std::int64_t t1 = t0 + p.seg_len < p.len ? t0 + p.seg_len : p.len;
+  bool d[NPL];
+  for (std::int64_t t = t0; t < t1; ++t) ln.stage(p.llr + t * BT, sig, d);
+  std::int32_t* col = p.mat + (static_cast<std::int64_t>(g) * p.s + j) * p.s;
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) {
+    const int i = r * 32 + lane;
+    if (i < p.s) col[i] = sig[r];
+  }
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(32) boundary_kernel(const SerialParams p) {
+  const int lane = threadIdx.x;
+  std::int64_t sig[NPL];
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) sig[r] = 0;  // sigma_0 = 0 (decoder.cpp:109)
+  for (int g = 0; g < p.nseg; ++g) {
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) {
+      if (r * 32 + lane < p.s) p.sig0[static_cast<std::int64_t>(g) * p.s + r * 32 + lane] = sig[r];
+    }
+    const std::int32_t* m = p.mat + static_cast<std::int64_t>(g) * p.s * p.s;
+    std::int64_t best[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) best[r] = LLONG_MIN;
+    for (int j = 0; j < p.s; ++j) {
+      const std::int64_t sj = __shfl_sync(kFull, sig[NPL == 1 ? 0 : (j >> 5)], j & 31);
+#pragma unroll
+      for (int r = 0; r < NPL; ++r) {
+        const int i = r * 32 + lane;
+        if (i < p.s) {
+          const std::int64_t c = static_cast<std::int64_t>(__ldg(m + static_cast<std::int64_t>(j) * p.s + i)) + sj;
+          best[r] = c > best[r] ? c : best[r];
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) sig[r] = best[r];
+  }
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) {
+    if (r * 32 + lane < p.s) p.sig0[static_cast<std::int64_t>(p.nseg) * p.s + r * 32 + lane] = sig[r];
+  }
+}
+
+template <int NPL, int BT>
+__global__ void __launch_bounds__(128) segment_forward_kernel(const SerialParams p) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (g >= p.nseg) return;
+  Lane<NPL, BT> ln;
+  ln.init(p, lane);
+  // exact start metrics minus a common offset (decisions depend on differences only)
+  const std::int64_t* s0 = p.sig0 + static_cast<std::int64_t>(g) * p.s;
+  const std::int64_t ref = s0[0];
+  std::int32_t sig[NPL];
+  bool valid[NPL];
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) {
+    const int i = r * 32 + lane;
+    valid[r] = i < p.s;
+    sig[r] = valid[r] ? static_cast<std::int32_t>(s0[i] - ref) : 0;
+  }
+  const std::int64_t t0 = static_cast<std::int64_t>(g) * p.seg_len;
+  const std::int64_t t1 = t0 + p.seg_len < p.len ? t0 + p.seg_len : p.len;
+  bool d[NPL];
+  for (std::int64_t t = t0; t < t1; ++t) {
+    ln.stage(p.llr + t * BT, sig, d);
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) {
+      const std::uint32_t w = __ballot_sync(kFull, d[r] && valid[r]);
+      if (lane == r) p.dec[t * NPL + r] = w;
+    }
+  }
+  if (g == p.nseg - 1) {
+    // final argmax, lowest state on ties (decoder.cpp:80-90)
+    std::int32_t bv = sig[0];
+    int bi = lane;
+    bool have = valid[0];
+#pragma unroll
+    for (int r = 1; r < NPL; ++r) {
+      if (valid[r] && (!have || sig[r] > bv)) {
+        bv = sig[r];
+        bi = r * 32 + lane;
+        have = true;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const std::int32_t ov = __shfl_xor_sync(kFull, bv, o);
+      const int oi = __shfl_xor_sync(kFull, bi, o);
+      const bool oh = __shfl_xor_sync(kFull, have ? 1 : 0, o) != 0;
+      if (oh && (!have || ov > bv || (ov == bv && oi < bi))) {
+        bv = ov;
+        bi = oi;
+        have = true;
+      }
+    }
+    if (lane == 0) p.endst[p.nseg] = bi;
+  }
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(128) segment_map_kernel(const SerialParams p) {
+  const int lane = threadIdx.x & 31;
+  const int g = blockIdx.x * 4 + (threadIdx.x >> 5);
+  if (g >= p.nseg) return;
+  const std::uint32_t lmask = static_cast<std::uint32_t>(p.s / 2 - 1);
+  const std::int64_t t0 = static_cast<std::int64_t>(g) * p.seg_len;
+  const std::int64_t t1 = t0 + p.seg_len < p.len ? t0 + p.seg_len : p.len;
+  std::uint32_t st[NPL];
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) st[r] = static_cast<std::uint32_t>((r * 32 + lane) % p.s);
+  for (std::int64_t t = t1 - 1; t >= t0; --t) {
+    std::uint32_t w[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) w[r] = __ldg(p.dec + t * NPL + r);
+#pragma unroll
+    for (int r = 0; r < NPL; ++r) {
+      std::uint32_t word = w[0];
+#pragma unroll
+      for (int q = 1; q < NPL; ++q) word = (st[r] >> 5) == static_cast<std::uint32_t>(q) ? w[q] : word;
+      st[r] = ((st[r] & lmask) << 1) | ((word >> (st[r] & 31)) & 1u);
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < NPL; ++r) {
+    if (r * 32 + lane < p.s) p.map[static_cast<std::int64_t>(g) * p.s + r * 32 + lane] = static_cast<std::int32_t>(st[r]);
+  }
+}
+
+__global__ void chain_kernel(const SerialParams p) {
+  int s = p.endst[p.nseg];
+  for (int g = p.nseg - 1; g >= 0; --g) {
+    p.endst[g] = s;
+    s = p.map[static_cast<std::int64_t>(g) * p.s + s];
+  }
+}
+
+template <int NPL>
+__global__ void __launch_bounds__(128) segment_emit_kernel(const SerialParams p) {
+  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  if (g >= p.nseg) return;
+  const std::uint32_t lmask = static_cast<std::uint32_t>(p.s / 2 - 1);
+  const int ksh = p.k - 2;
+  const std::int64_t t0 = static_cast<std::int64_t>(g) * p.seg_len;
+  const std::int64_t t1 = t0 + p.seg_len < p.len ? t0 + p.seg_len : p.len;
+  std::uint32_t state = static_cast<std::uint32_t>(p.endst[g]);
+  std::uint32_t acc = 0;
+  std::int64_t cur = -1;
+  for (std::int64_t t = t1 - 1; t >= t0; --t) {
+    if (t >= p.emit_lo && t < p.emit_hi) {
+      const std::int64_t bit = p.out_bit0 + t;
+      const std::int64_t w = bit >> 5;
+      if (w != cur) {
+        if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+        cur = w;
+        acc = 0;
+      }
+      acc |= (state >> ksh) << (bit & 31);
+    }
+    const std::uint32_t word = __ldg(p.dec + t * NPL + (NPL > 1 ? (state >> 5) : 0));
+    state = ((state & lmask) << 1) | ((word >> (state & 31)) & 1u);
+  }
+  if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+}
+
+template <int NPL, int BT>
+cudaError_t run(SerialParams p, cudaStream_t s) {
+  const std::size_t S = static_cast<std::size_t>(p.s);
+  const std::size_t bytes = sizeof(std::int32_t) * p.nseg * S * S + sizeof(std::int64_t) * (p.nseg + 1) * S +
+                            sizeof(std::uint32_t) * p.len * NPL + sizeof(std::int32_t) * (p.nseg * S + p.nseg + 1) + 64;
+  unsigned char* buf = nullptr;
+  if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&buf), bytes, s); e != cudaSuccess) return e;
+  unsigned char* q = buf;
+  p.mat = reinterpret_cast<std::int32_t*>(q);
+  q += sizeof(std::int32_t) * p.nseg * S * S;
+  p.sig0 = reinterpret_cast<std::int64_t*>(q);
+  q += sizeof(std::int64_t) * (p.nseg + 1) * S;
+  p.dec = reinterpret_cast<std::uint32_t*>(q);
+  q += sizeof(std::uint32_t) * p.len * NPL;
+  p.map = reinterpret_cast<std::int32_t*>(q);
+  q += sizeof(std::int32_t) * p.nseg * S;
+  p.endst = reinterpret_cast<std::int32_t*>(q);
+  const std::int64_t warpsA = static_cast<std::int64_t>(p.nseg) * p.s;
+  segment_matrix_kernel<NPL, BT><<<static_cast<unsigned>((warpsA + 3) / 4), 128, 0, s>>>(p);
+  boundary_kernel<NPL><<<1, 32, 0, s>>>(p);
+  segment_forward_kernel<NPL, BT><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
+  segment_map_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
+  chain_kernel<<<1, 1, 0, s>>>(p);
+  segment_emit_kernel<NPL><<<static_cast<unsigned>((p.nseg + 127) / 128), 128, 0, s>>>(p);
+  cudaError_t e = cudaGetLastError();
+  const cudaError_t ef = cudaFreeAsync(buf, s);
+  return e != cudaSuccess ? e : ef;
+}
+
+}  // namespace
+
+bool serial_parallel_supported(const DecodeLaunch& p) {
+  if (p.s < 4 || p.s > 64 || (p.b != 2 && p.b != 3)) return false;
+  if (p.frame_end - p.frame_begin != 1 || p.nblocks > 0 || p.frame_list || p.sigma) return false;
+  if (p.f0 > 0 && p.f0 < p.f) return false;  // one traceback per frame
+  const FrameGeom g(p.frame_begin, p.n, p.f, p.v1, p.v2, p.f0);
+  return g.len() >= 8192;
+}
+
+cudaError_t launch_serial_parallel_i8(const DecodeLaunch& p, cudaStream_t stream) {
+  const FrameGeom g(p.frame_begin, p.n, p.f, p.v1, p.v2, p.f0);
+  SerialParams sp{};
+  sp.llr = static_cast<const std::int8_t*>(p.llr) + (g.beg - p.llr_stage0) * p.b;
+  sp.k = p.k;
+  sp.b = p.b;
+  sp.s = p.s;
+  sp.len = g.len();
+  // segments: enough of them to fill the GPU in kernel A, short enough for
+  // the sequential kernels B and D2
+  std::int64_t seg = 512;
+  while (seg < 8192 && (sp.len + seg - 1) / seg > 1024) seg *= 2;
+  sp.seg_len = static_cast<int>(seg);
+  sp.nseg = static_cast<int>((sp.len + seg - 1) / seg);
+  sp.in_out = p.in_out;
+  sp.out = p.out;
+  sp.out_bit0 = g.beg - p.out_stage0;
+  sp.emit_lo = g.out_lo - g.beg;
+  sp.emit_hi = g.out_hi - g.beg;
+  const int npl = p.s > 32 ? 2 : 1;
+  if (npl == 2) return p.b == 2 ? run<2, 2>(sp, stream) : run<2, 3>(sp, stream);
+  return p.b == 2 ? run<1, 2>(sp, stream) : run<1, 3>(sp, stream);
+}
+
+}  // namespace vd

@@ -356,3 +356,32 @@ def test_long_frames_full_size_sampled_windows(port):
             exp, _, _ = port.framed_decode(*K7, q[lo * 2:hi * 2], hi - lo, f, v1, v2)
             a, b2 = (m0 - g0) * f, (m1 - g0) * f
             assert np.array_equal(got_all[m0 * f:m1 * f], exp[a:b2]), (cfg, m0)
+
+
+@pytest.mark.parametrize("code", [K7, (7, 3, [0o133, 0o171, 0o165]), (3, 2, [7, 5]), (5, 2, [0o23, 0o35]),
+                                  (6, 2, [0o53, 0o75]), (4, 3, [0o13, 0o15, 0o17])],
+                         ids=lambda c: f"K{c[0]}B{c[1]}")
+def test_serial_decode_segment_parallel(code, port):
+    """Long single frames (serial_decode, f >= N) take the exact segment-
+    parallel decoder (max-plus transfer matrices per segment, sequential
+    boundary combine, per-segment re-run + traceback): bit-identical to the
+    oracle, including tie-heavy inputs (scale 1 -> LLRs in {-1, 0, 1})."""
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng(31 + k * b)
+    for n, scale in ((8192, 32.0), (8193, 4.0), (65543, 1.0), (300_001, 32.0)):
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(0, 3)), n + k)
+        q = oracle.quantize(rx, scale)
+        exp = port.serial_decode(k, b, polys, q.astype(np.float64), n)
+        out = vd.serial_decode(block(q, b), t)
+        bad = np.flatnonzero(out.bits != exp)
+        assert bad.size == 0, (code, n, scale, bad[:10], bad.size)
+        assert (out.stats.frames, out.stats.stages, out.stats.tracebacks) == (1, n, 1)
+    # one long frame with overlaps inside a longer stream (f >= n - ... : single frame, clipped window)
+    n = 50_000
+    rx, _ = port.gen_bench_block(k, b, polys, n, 2.0, 99)
+    q = oracle.quantize(rx, 32.0)
+    cfg = vd.FrameConfig(60_000, 0, 0)
+    exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2)
+    packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+    assert np.array_equal(vd.unpack_bits(packed, n), exp)
