@@ -8,16 +8,17 @@
 //      the forward pass from the unit vector e_j (0 at j, -inf elsewhere)
 //      gives column j of the segment transfer matrix M_g (M_g[i][j] = best
 //      metric of a path j -> i through the segment). No decisions.
-//   B  boundary_kernel        one warp, sequential over segments:
-//      sigma_{g+1} = M_g (x) sigma_g (64 x 64 max-plus mat-vec, int64).
+//   B  boundary_kernel        one CTA, sequential over segments:
+//      sigma_{g+1} = M_g (x) sigma_g (64 x 64 max-plus mat-vec, int64; the
+//      next matrix is prefetched while the current one is reduced).
 //   C  segment_forward_kernel per segment (one warp each): the ordinary
 //      forward pass from the exact sigma_g, storing the decision words; the
 //      last segment also takes the argmax of the final metrics (lowest state
 //      on ties, decoder.cpp:80-90).
 //   D1 segment_map_kernel     per segment: trace back from every end state
 //      through the segment (one chain per state) -> map_g[state].
-//   D2 chain_kernel           one thread: end state of every segment by
-//      composing the maps from the final argmax.
+//   D2 chain_kernel           one warp: end state of every segment by
+//      composing the maps from the final argmax (maps prefetched 8 ahead).
 //   D3 segment_emit_kernel    per segment: trace back from its end state and
 //      write its decoded bits.
 //
@@ -149,39 +150,57 @@ __global__ void __launch_bounds__(128) segment_matrix_kernel(const SerialParams 
   }
 }
 
-template <int NPL>
-__global__ void __launch_bounds__(32) boundary_kernel(const SerialParams p) {
-  const int lane = threadIdx.x;
-  std::int64_t sig[NPL];
+// 256 threads: thread (q, i) = (tid >> 6, tid & 63) takes row i over the
+// columns j = q, q + 4, ...; the next segment's matrix is prefetched into
+// registers while the current one is reduced from shared memory.
+__global__ void __launch_bounds__(256) boundary_kernel(const SerialParams p) {
+  __shared__ std::int32_t m_s[2][64 * 64];
+  __shared__ std::int64_t sig_s[64];
+  __shared__ std::int64_t part[4][64];
+  const int tid = threadIdx.x;
+  const int i = tid & 63, q = tid >> 6;
+  const int S = p.s, SS = S * S;
+  constexpr int kPer = 64 * 64 / 256;  // matrix elements each thread moves
+  if (tid < 64) sig_s[tid] = 0;        // sigma_0 = 0 (decoder.cpp:109)
+  std::int32_t pre[kPer];
+  auto load = [&](int g) {
+    const std::int32_t* m = p.mat + static_cast<std::int64_t>(g) * SS;
 #pragma unroll
-  for (int r = 0; r < NPL; ++r) sig[r] = 0;  // sigma_0 = 0 (decoder.cpp:109)
-  for (int g = 0; g < p.nseg; ++g) {
-#pragma unroll
-    for (int r = 0; r < NPL; ++r) {
-      if (r * 32 + lane < p.s) p.sig0[static_cast<std::int64_t>(g) * p.s + r * 32 + lane] = sig[r];
+    for (int k = 0; k < kPer; ++k) {
+      const int e = tid + 256 * k;
+      pre[k] = e < SS ? __ldg(m + e) : 0;
     }
-    const std::int32_t* m = p.mat + static_cast<std::int64_t>(g) * p.s * p.s;
-    std::int64_t best[NPL];
+  };
+  auto stash = [&](int buf) {
 #pragma unroll
-    for (int r = 0; r < NPL; ++r) best[r] = LLONG_MIN;
-    for (int j = 0; j < p.s; ++j) {
-      const std::int64_t sj = __shfl_sync(kFull, sig[NPL == 1 ? 0 : (j >> 5)], j & 31);
-#pragma unroll
-      for (int r = 0; r < NPL; ++r) {
-        const int i = r * 32 + lane;
-        if (i < p.s) {
-          const std::int64_t c = static_cast<std::int64_t>(__ldg(m + static_cast<std::int64_t>(j) * p.s + i)) + sj;
-          best[r] = c > best[r] ? c : best[r];
-        }
+    for (int k = 0; k < kPer; ++k) m_s[buf][tid + 256 * k] = pre[k];
+  };
+  load(0);
+  stash(0);
+  __syncthreads();
+  for (int g = 0; g < p.nseg; ++g) {
+    if (g + 1 < p.nseg) load(g + 1);  // in flight during this segment's reduction
+    if (tid < S) p.sig0[static_cast<std::int64_t>(g) * S + tid] = sig_s[tid];
+    std::int64_t best = LLONG_MIN;
+    if (i < S) {
+      const std::int32_t* m = m_s[g & 1];
+      for (int j = q; j < S; j += 4) {
+        const std::int64_t c = static_cast<std::int64_t>(m[j * S + i]) + sig_s[j];
+        best = c > best ? c : best;
       }
     }
+    part[q][i] = best;
+    __syncthreads();
+    if (tid < S) {
+      std::int64_t b = part[0][tid];
 #pragma unroll
-    for (int r = 0; r < NPL; ++r) sig[r] = best[r];
+      for (int k = 1; k < 4; ++k) b = part[k][tid] > b ? part[k][tid] : b;
+      sig_s[tid] = b;
+    }
+    if (g + 1 < p.nseg) stash((g + 1) & 1);
+    __syncthreads();
   }
-#pragma unroll
-  for (int r = 0; r < NPL; ++r) {
-    if (r * 32 + lane < p.s) p.sig0[static_cast<std::int64_t>(p.nseg) * p.s + r * 32 + lane] = sig[r];
-  }
+  if (tid < S) p.sig0[static_cast<std::int64_t>(p.nseg) * S + tid] = sig_s[tid];
 }
 
 template <int NPL, int BT>
@@ -270,18 +289,47 @@ __global__ void __launch_bounds__(128) segment_map_kernel(const SerialParams p) 
   }
 }
 
-__global__ void chain_kernel(const SerialParams p) {
+// one warp: the segment maps are fetched kDepth segments ahead (independent
+// of the chained state) into a register ring; the state hops by shuffles.
+__global__ void __launch_bounds__(32) chain_kernel(const SerialParams p) {
+  constexpr int kDepth = 8;
+  const int lane = threadIdx.x;
+  std::int32_t ring[kDepth][2];
+  auto fetch = [&](int g, std::int32_t (&m)[2]) {
+    if (g < 0) return;
+    const std::int32_t* row = p.map + static_cast<std::int64_t>(g) * p.s;
+    m[0] = lane < p.s ? __ldg(row + lane) : 0;
+    m[1] = lane + 32 < p.s ? __ldg(row + lane + 32) : 0;
+  };
   int s = p.endst[p.nseg];
-  for (int g = p.nseg - 1; g >= 0; --g) {
-    p.endst[g] = s;
-    s = p.map[static_cast<std::int64_t>(g) * p.s + s];
+  const int top = p.nseg - 1;
+#pragma unroll
+  for (int d = 0; d < kDepth; ++d) fetch(top - d, ring[d]);
+  for (int g0 = top; g0 >= 0; g0 -= kDepth) {
+#pragma unroll
+    for (int d = 0; d < kDepth; ++d) {
+      const int g = g0 - d;
+      if (g >= 0) {
+        if (lane == 0) p.endst[g] = s;
+        const std::int32_t a = __shfl_sync(kFull, ring[d][0], s & 31), b = __shfl_sync(kFull, ring[d][1], s & 31);
+        s = (s >> 5) ? b : a;
+        fetch(g - kDepth, ring[d]);  // refill this slot for the next round
+      }
+    }
   }
 }
 
+// one warp per segment: the segment's decision words are staged into shared
+// memory in chunks (coalesced), lane 0 walks them with 8 stages of words in
+// registers (no load on the state chain) and writes whole output words.
+constexpr int kEmitChunk = 1024;
 template <int NPL>
 __global__ void __launch_bounds__(128) segment_emit_kernel(const SerialParams p) {
-  const int g = blockIdx.x * blockDim.x + threadIdx.x;
+  __shared__ std::uint32_t tb_all[4][kEmitChunk * NPL];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int g = blockIdx.x * 4 + w;
   if (g >= p.nseg) return;
+  std::uint32_t* tb = tb_all[w];
   const std::uint32_t lmask = static_cast<std::uint32_t>(p.s / 2 - 1);
   const int ksh = p.k - 2;
   const std::int64_t t0 = static_cast<std::int64_t>(g) * p.seg_len;
@@ -289,21 +337,46 @@ __global__ void __launch_bounds__(128) segment_emit_kernel(const SerialParams p)
   std::uint32_t state = static_cast<std::uint32_t>(p.endst[g]);
   std::uint32_t acc = 0;
   std::int64_t cur = -1;
-  for (std::int64_t t = t1 - 1; t >= t0; --t) {
+  auto step = [&](std::int64_t t, std::uint32_t word) {
     if (t >= p.emit_lo && t < p.emit_hi) {
       const std::int64_t bit = p.out_bit0 + t;
-      const std::int64_t w = bit >> 5;
-      if (w != cur) {
+      const std::int64_t wd = bit >> 5;
+      if (wd != cur) {
         if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
-        cur = w;
+        cur = wd;
         acc = 0;
       }
       acc |= (state >> ksh) << (bit & 31);
     }
-    const std::uint32_t word = __ldg(p.dec + t * NPL + (NPL > 1 ? (state >> 5) : 0));
     state = ((state & lmask) << 1) | ((word >> (state & 31)) & 1u);
+  };
+  for (std::int64_t chi = t1 - 1; chi >= t0; chi -= kEmitChunk) {
+    const std::int64_t clo = chi - kEmitChunk + 1 > t0 ? chi - kEmitChunk + 1 : t0;
+    const int cnt = static_cast<int>(chi - clo + 1) * NPL;
+    __syncwarp();
+    for (int i = lane; i < cnt; i += 32) tb[i] = __ldg(p.dec + clo * NPL + i);
+    __syncwarp();
+    if (lane == 0) {
+      std::int64_t t = chi;
+      for (; t - 7 >= clo; t -= 8) {
+        std::uint32_t wv[8][NPL];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+#pragma unroll
+          for (int r = 0; r < NPL; ++r) wv[u][r] = tb[(t - u - clo) * NPL + r];
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          std::uint32_t word = wv[u][0];
+#pragma unroll
+          for (int r = 1; r < NPL; ++r) word = (state >> 5) == static_cast<std::uint32_t>(r) ? wv[u][r] : word;
+          step(t - u, word);
+        }
+      }
+      for (; t >= clo; --t) step(t, tb[(t - clo) * NPL + (NPL > 1 ? (state >> 5) : 0)]);
+    }
   }
-  if (cur >= 0 && acc) atomicOr(p.out + cur, acc);
+  if (lane == 0 && cur >= 0 && acc) atomicOr(p.out + cur, acc);
 }
 
 template <int NPL, int BT>
@@ -325,11 +398,11 @@ cudaError_t run(SerialParams p, cudaStream_t s) {
   p.endst = reinterpret_cast<std::int32_t*>(q);
   const std::int64_t warpsA = static_cast<std::int64_t>(p.nseg) * p.s;
   segment_matrix_kernel<NPL, BT><<<static_cast<unsigned>((warpsA + 3) / 4), 128, 0, s>>>(p);
-  boundary_kernel<NPL><<<1, 32, 0, s>>>(p);
+  boundary_kernel<<<1, 256, 0, s>>>(p);
   segment_forward_kernel<NPL, BT><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
   segment_map_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
-  chain_kernel<<<1, 1, 0, s>>>(p);
-  segment_emit_kernel<NPL><<<static_cast<unsigned>((p.nseg + 127) / 128), 128, 0, s>>>(p);
+  chain_kernel<<<1, 32, 0, s>>>(p);
+  segment_emit_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
   const cudaError_t ef = cudaFreeAsync(buf, s);
   return e != cudaSuccess ? e : ef;
@@ -356,7 +429,7 @@ cudaError_t launch_serial_parallel_i8(const DecodeLaunch& p, cudaStream_t stream
   // segments: enough of them to fill the GPU in kernel A, short enough for
   // the sequential kernels B and D2
   std::int64_t seg = 512;
-  while (seg < 8192 && (sp.len + seg - 1) / seg > 1024) seg *= 2;
+  while (seg < 16384 && (sp.len + seg - 1) / seg > 1024) seg *= 2;
   sp.seg_len = static_cast<int>(seg);
   sp.nseg = static_cast<int>((sp.len + seg - 1) / seg);
   sp.in_out = p.in_out;
