@@ -260,6 +260,7 @@ vd_status decode_device(const vd_code* code, const vd_frame_cfg* cfg, std::int64
   if (vd_status st = device_table(code, dev, &in_out)) return st;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
 
+  VD_CUDA(vd::retain_async_pool(), "memory pool");
   // Zero the output words the frames touch; kernels OR bits into them.
   const std::int64_t w0 = (g0.out_lo - out_stage0) / 32;
   const std::int64_t w1 = (g1.out_hi - out_stage0 + 31) / 32;
@@ -463,6 +464,7 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
   std::memcpy(host_p + i32_off, ilo.data(), sizeof(std::int32_t) * nblocks);
   std::memcpy(host_p + i32_off + sizeof(std::int32_t) * nb1, ihi.data(), sizeof(std::int32_t) * nblocks);
   unsigned char* dscratch = nullptr;
+  VD_CUDA(vd::retain_async_pool(), "memory pool");
   VD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dscratch), bytes, s), "cudaMallocAsync(batch tables)");
   VD_CUDA(cudaMemcpyAsync(dscratch, host_p, bytes, cudaMemcpyHostToDevice, s), "upload batch tables");
   if (!pinned_done) VD_CUDA(cudaEventCreateWithFlags(&pinned_done, cudaEventDisableTiming), "cudaEventCreate");
@@ -742,6 +744,21 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
 }  // namespace
 
 namespace vd {
+cudaError_t retain_async_pool() {
+  static std::mutex mu;
+  static std::map<int, bool> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done[dev]) return cudaSuccess;
+  cudaMemPool_t pool;
+  if (cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev); e != cudaSuccess) return e;
+  std::uint64_t thr = ~0ull;
+  if (cudaError_t e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr); e != cudaSuccess) return e;
+  done[dev] = true;
+  return cudaSuccess;
+}
+
 int sm_count() {
   static std::mutex mu;
   static std::map<int, int> cache;

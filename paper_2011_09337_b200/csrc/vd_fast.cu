@@ -1183,23 +1183,6 @@ inline SideStream* side_stream() {
   return &(cache.m[dev] = ss);
 }
 
-// The device's default memory pool keeps freed blocks (release threshold =
-// max) so the per-launch cudaMallocAsync of the spill scratch is a pool hit.
-inline cudaError_t scratch_pool() {
-  static std::mutex mu;
-  static std::map<int, bool> done;
-  int dev = 0;
-  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
-  std::lock_guard<std::mutex> lk(mu);
-  if (done[dev]) return cudaSuccess;
-  cudaMemPool_t pool;
-  if (cudaError_t e = cudaDeviceGetDefaultMemPool(&pool, dev); e != cudaSuccess) return e;
-  std::uint64_t thr = ~0ull;
-  if (cudaError_t e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr); e != cudaSuccess) return e;
-  done[dev] = true;
-  return cudaSuccess;
-}
-
 struct Plan {
   FastParams fp;
   std::size_t smem;
@@ -1360,7 +1343,7 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   if (pad) {
     constexpr int B = GEO::B;
     const std::int64_t stages = head_end * p.f + p.v2;  // window end of the last head frame (<= n: mi1 >= head_end)
-    if (cudaError_t e = scratch_pool(); e != cudaSuccess) return e;
+    if (cudaError_t e = retain_async_pool(); e != cudaSuccess) return e;
     // (+16 bytes: the last LLR word of a window may extend past the window's last stage)
     if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&head_buf), (p.v1 + stages + kPfSlackStages) * B + 16,
                                         stream);
@@ -1415,9 +1398,9 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
   blocks = std::min<std::int64_t>(blocks, static_cast<std::int64_t>(sm_count()) * per_sm);
   if (fp.g_rows > 0) {
     // stream-ordered scratch for the spilled survivor rows (the pool keeps it
-    // cached across launches, see scratch_pool())
+    // cached across launches, see retain_async_pool())
     const std::size_t bytes = static_cast<std::size_t>(blocks) * fp.warps_per_cta * fp.g_rows * 32 * 4;
-    if (cudaError_t ea = scratch_pool(); ea != cudaSuccess) return ea;
+    if (cudaError_t ea = retain_async_pool(); ea != cudaSuccess) return ea;
     if (cudaError_t ea = cudaMallocAsync(reinterpret_cast<void**>(&fpl.gscratch), bytes, stream); ea != cudaSuccess)
       return ea;
   }

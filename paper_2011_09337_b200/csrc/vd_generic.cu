@@ -34,6 +34,9 @@ namespace {
 constexpr int kWarps = 4;     // warps (frames in flight) per CTA
 constexpr int kStage = 128;   // LLR staging depth (stages) per warp
 constexpr int kTbChunk = 512; // traceback staging chunk (stages) for decisions held in global memory
+#ifndef VD_TB1_SMEM
+#define VD_TB1_SMEM 0  // 1: single-traceback walk also for shared-memory decisions (measured: FP64 3.6x slower)
+#endif
 constexpr unsigned kFull = 0xffffffffu;
 
 struct GenericParams {
@@ -445,7 +448,8 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
     // The decision words of 4 stages are loaded before the state chain walks
     // them, so the chain is select + shift instead of a load per stage.
     const std::uint32_t lmask = static_cast<std::uint32_t>(S / 2 - 1);
-    if (g.num_sub == 1) {
+    const bool tb1 = g.num_sub == 1 && (VD_TB1_SMEM || !gp.dec_in_smem);
+    if (tb1) {
       // One traceback per frame (f0 == 0, serial_decode): lane 0 walks from
       // the stored-max state with the decision words of 8 stages loaded ahead
       // (they do not depend on the traced path), so the state chain is pure
@@ -503,7 +507,7 @@ __global__ void __launch_bounds__(kWarps * 32) reg_kernel(const GenericParams gp
         }
       }
     }
-    for (std::int64_t s = lane; s < g.num_sub && g.num_sub > 1; s += 32) {
+    for (std::int64_t s = lane; s < g.num_sub && !tb1; s += 32) {
       const std::int64_t st = g.start_stage(s, p.v2);
       const std::int64_t lo = g.sub_lo(s), hi = g.sub_hi(s);
       std::uint32_t state;

@@ -130,4 +130,9 @@ cudaError_t launch_count_bit_errors(const std::uint32_t* a, const std::uint32_t*
 /// SM count of the current device (cached per device).
 int sm_count();
 
+/// Makes the current device's default memory pool keep freed blocks (release
+/// threshold = max), so the per-launch stream-ordered scratch allocations
+/// (cudaMallocAsync) of the kernels are pool hits instead of fresh mappings.
+cudaError_t retain_async_pool();
+
 }  // namespace vd
