@@ -38,6 +38,10 @@
 namespace vd {
 namespace {
 
+#ifndef VD_SERIAL_COLS
+#define VD_SERIAL_COLS 1
+#endif
+
 constexpr unsigned kFull = 0xffffffffu;
 constexpr std::int32_t kNeg = -(1 << 28);  // "-inf" for the unit start vectors
 
@@ -47,6 +51,7 @@ struct SerialParams {
   std::int64_t len;        // window stages
   int seg_len, nseg;
   const std::uint32_t* in_out;
+  std::uint32_t polys[4];
   std::int32_t* mat;       // [nseg][S (j)][S (i)]: column-major per segment
   std::int64_t* sig0;      // [nseg + 1][S]: metrics before each segment
   std::uint32_t* dec;      // [len][NPL] decision words
@@ -148,6 +153,96 @@ __global__ void __launch_bounds__(128) segment_matrix_kernel(const SerialParams 
     const int i = r * 32 + lane;
     if (i < p.s) col[i] = sig[r];
   }
+}
+
+// Kernel A for codes known at compile time (the common standards): one LANE
+// per column j — all S states of the column live in the lane's registers, so
+// a stage is S x (IADD3 + VIADDMNMX-style max) with compile-time branch-table
+// picks and no shuffles (the stage's LLRs and table are warp-uniform): ~2
+// instructions per column-state instead of ~18 for the warp-per-column form.
+template <int K_, int B_, std::uint32_t P0, std::uint32_t P1, std::uint32_t P2 = 0>
+struct SCode {
+  static constexpr int K = K_, B = B_, S = 1 << (K_ - 1);
+  static constexpr std::uint32_t poly(int i) { return i == 0 ? P0 : i == 1 ? P1 : P2; }
+  // branch output of (state s, input u), polys[0] at the MSB (trellis.cpp:65-79)
+  static constexpr std::uint32_t out(std::uint32_t st, std::uint32_t u) {
+    const std::uint32_t reg = (u << (K - 1)) | st;
+    std::uint32_t bo = 0;
+    for (int b = 0; b < B; ++b) {
+      std::uint32_t x = poly(b) & reg, par = 0;
+      while (x) {
+        par ^= x & 1u;
+        x >>= 1;
+      }
+      bo |= par << (B - 1 - b);
+    }
+    return bo;
+  }
+  // incoming output of state j from predecessor w (trellis.cpp:81-91)
+  static constexpr std::uint32_t in_out(int j, int w) {
+    const std::uint32_t pred = 2u * (static_cast<std::uint32_t>(j) & (S / 2 - 1)) + static_cast<std::uint32_t>(w);
+    return out(pred, static_cast<std::uint32_t>(j) >> (K - 2));
+  }
+  static bool matches(int k, int b, const std::uint32_t* p) {
+    if (k != K || b != B) return false;
+    for (int i = 0; i < B; ++i) {
+      if (p[i] != poly(i)) return false;
+    }
+    return true;
+  }
+};
+
+template <class C>
+__global__ void __launch_bounds__(64) segment_matrix_cols_kernel(const SerialParams p) {
+  constexpr int S = C::S, B = C::B, NT = 1 << (B - 1);
+  constexpr std::uint32_t half = 1u << (B - 1), tmask = (1u << B) - 1u;
+  const std::int64_t col = static_cast<std::int64_t>(blockIdx.x) * 64 + threadIdx.x;  // g * S + j
+  if (col >= static_cast<std::int64_t>(p.nseg) * S) return;
+  const int g = static_cast<int>(col / S), j = static_cast<int>(col % S);
+  std::int32_t sig[S];
+#pragma unroll
+  for (int i = 0; i < S; ++i) sig[i] = i == j ? 0 : kNeg;
+  const std::int64_t t0 = static_cast<std::int64_t>(g) * p.seg_len;
+  const std::int64_t t1 = t0 + p.seg_len < p.len ? t0 + p.seg_len : p.len;
+  // one stage: sig <- A_t (x) sig (values only; ties do not matter here)
+  auto stage = [&](std::int64_t t) {
+    const std::int8_t* l = p.llr + t * B;
+    std::int32_t v[B];
+#pragma unroll
+    for (int i = 0; i < B; ++i) v[i] = l[i];
+    std::int32_t T[NT];
+#pragma unroll
+    for (int x = 0; x < NT; ++x) {
+      std::int32_t acc = 0;
+#pragma unroll
+      for (int i = 0; i < B; ++i) acc += ((x >> (B - 1 - i)) & 1) ? -v[i] : v[i];
+      T[x] = acc;
+    }
+    std::int32_t ns[S];
+#pragma unroll
+    for (int jj = 0; jj < S; ++jj) {
+      const int m = jj & (S / 2 - 1);
+      const std::uint32_t x0 = C::in_out(jj, 0), x1 = C::in_out(jj, 1);
+      const std::int32_t b0 = x0 >= half ? -T[(x0 ^ tmask)] : T[x0];
+      const std::int32_t b1 = x1 >= half ? -T[(x1 ^ tmask)] : T[x1];
+      const std::int32_t s1 = sig[2 * m] + b0, s2 = sig[2 * m + 1] + b1;
+      ns[jj] = s1 > s2 ? s1 : s2;
+    }
+#pragma unroll
+    for (int jj = 0; jj < S; ++jj) sig[jj] = ns[jj];
+  };
+  // K-1 stages compose the perfect shuffle to the identity, so an unrolled
+  // group of K-1 stages needs no register moves
+  constexpr int U = C::K - 1;
+  std::int64_t t = t0;
+  for (; t + U <= t1; t += U) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) stage(t + u);
+  }
+  for (; t < t1; ++t) stage(t);
+  std::int32_t* dst = p.mat + col * S;  // column j of segment g: rows i contiguous
+#pragma unroll
+  for (int i = 0; i < S; i += 4) *reinterpret_cast<int4*>(dst + i) = make_int4(sig[i], sig[i + 1], sig[i + 2], sig[i + 3]);
 }
 
 // 256 threads: thread (q, i) = (tid >> 6, tid & 63) takes row i over the
@@ -379,6 +474,33 @@ __global__ void __launch_bounds__(128) segment_emit_kernel(const SerialParams p)
   if (lane == 0 && cur >= 0 && acc) atomicOr(p.out + cur, acc);
 }
 
+using SK7a = SCode<7, 2, 0171, 0133>;
+using SK7b = SCode<7, 2, 0133, 0171>;
+using SK7c = SCode<7, 3, 0133, 0171, 0165>;
+using SK5a = SCode<5, 2, 023, 035>;
+using SK6a = SCode<6, 2, 053, 075>;
+using SK3a = SCode<3, 2, 07, 05>;
+
+// register-column kernel A for the compile-time codes; false -> caller uses the generic one
+bool launch_cols(const SerialParams& p, cudaStream_t s) {
+  if (!VD_SERIAL_COLS) return false;
+  const std::int64_t cols = static_cast<std::int64_t>(p.nseg) * p.s;
+  const unsigned grid = static_cast<unsigned>((cols + 63) / 64);
+#define VD_TRY_COLS(C)                                                   \
+  if (C::matches(p.k, p.b, p.polys)) {                                   \
+    segment_matrix_cols_kernel<C><<<grid, 64, 0, s>>>(p);                \
+    return true;                                                         \
+  }
+  VD_TRY_COLS(SK7a)
+  VD_TRY_COLS(SK7b)
+  VD_TRY_COLS(SK7c)
+  VD_TRY_COLS(SK5a)
+  VD_TRY_COLS(SK6a)
+  VD_TRY_COLS(SK3a)
+#undef VD_TRY_COLS
+  return false;
+}
+
 template <int NPL, int BT>
 cudaError_t run(SerialParams p, cudaStream_t s) {
   const std::size_t S = static_cast<std::size_t>(p.s);
@@ -397,7 +519,7 @@ cudaError_t run(SerialParams p, cudaStream_t s) {
   q += sizeof(std::int32_t) * p.nseg * S;
   p.endst = reinterpret_cast<std::int32_t*>(q);
   const std::int64_t warpsA = static_cast<std::int64_t>(p.nseg) * p.s;
-  segment_matrix_kernel<NPL, BT><<<static_cast<unsigned>((warpsA + 3) / 4), 128, 0, s>>>(p);
+  if (!launch_cols(p, s)) segment_matrix_kernel<NPL, BT><<<static_cast<unsigned>((warpsA + 3) / 4), 128, 0, s>>>(p);
   boundary_kernel<<<1, 256, 0, s>>>(p);
   segment_forward_kernel<NPL, BT><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
   segment_map_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
@@ -433,6 +555,7 @@ cudaError_t launch_serial_parallel_i8(const DecodeLaunch& p, cudaStream_t stream
   sp.seg_len = static_cast<int>(seg);
   sp.nseg = static_cast<int>((sp.len + seg - 1) / seg);
   sp.in_out = p.in_out;
+  for (int i = 0; i < 4 && i < p.b; ++i) sp.polys[i] = p.polys[i];
   sp.out = p.out;
   sp.out_bit0 = g.beg - p.out_stage0;
   sp.emit_lo = g.out_lo - g.beg;
