@@ -14,6 +14,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "vd_common.cuh"
@@ -580,6 +581,15 @@ struct DevCtx {
   std::size_t out_cap[2] = {0, 0};
   void* pun[2] = {nullptr, nullptr};  // punctured-stream staging (depuncture input)
   std::size_t pun_cap[2] = {0, 0};
+  // pinned host staging for pageable caller buffers (input chunks / output words)
+  void* hin[2] = {nullptr, nullptr};
+  std::size_t hin_cap[2] = {0, 0};
+  void* hout[2] = {nullptr, nullptr};
+  std::size_t hout_cap[2] = {0, 0};
+  cudaEvent_t hin_free[2] = {nullptr, nullptr}, hout_ready[2] = {nullptr, nullptr};
+  bool hin_used[2] = {false, false}, hout_pending[2] = {false, false};
+  std::uint32_t* pend_dst[2] = {nullptr, nullptr};
+  std::size_t pend_bytes[2] = {0, 0};
 };
 
 struct ThreadCtx {
@@ -591,6 +601,10 @@ struct ThreadCtx {
         if (kv.second.llr[i]) cudaFree(kv.second.llr[i]);
         if (kv.second.out[i]) cudaFree(kv.second.out[i]);
         if (kv.second.pun[i]) cudaFree(kv.second.pun[i]);
+        if (kv.second.hin[i]) cudaFreeHost(kv.second.hin[i]);
+        if (kv.second.hout[i]) cudaFreeHost(kv.second.hout[i]);
+        if (kv.second.hin_free[i]) cudaEventDestroy(kv.second.hin_free[i]);
+        if (kv.second.hout_ready[i]) cudaEventDestroy(kv.second.hout_ready[i]);
         if (kv.second.st[i]) cudaStreamDestroy(kv.second.st[i]);
       }
     }
@@ -612,6 +626,45 @@ vd_status ensure(void** p, std::size_t* cap, std::size_t bytes) {
 struct Chunk {
   std::int64_t f0, f1;  // frame range
 };
+
+// Page-locked host memory reaches full PCIe rate with async copies; pageable
+// caller buffers (numpy arrays, std::vector, Eigen blocks) are staged through
+// per-(thread, device) pinned buffers, the host copy split over a few threads.
+bool host_pinned(const void* ptr) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
+
+void parallel_memcpy(void* dst, const void* src, std::size_t bytes) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const std::size_t nt = bytes < (std::size_t{8} << 20) ? 1 : std::min<std::size_t>(8, std::max(1u, hw / 2));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const std::size_t part = (bytes + nt - 1) / nt;
+  std::vector<std::thread> th;
+  for (std::size_t i = 1; i < nt; ++i) {
+    const std::size_t lo = i * part, len = lo < bytes ? std::min(part, bytes - lo) : 0;
+    if (len) th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, len); });
+  }
+  std::memcpy(dst, src, std::min(part, bytes));
+  for (auto& t : th) t.join();
+}
+
+vd_status ensure_host(void** p, std::size_t* cap, std::size_t bytes) {
+  if (*cap >= bytes) return VD_OK;
+  if (*p) cudaFreeHost(*p);
+  *p = nullptr;
+  *cap = 0;
+  VD_CUDA(cudaMallocHost(p, bytes), "cudaMallocHost(staging)");
+  *cap = bytes;
+  return VD_OK;
+}
 
 // pp != nullptr (int8 only): `llr` is the PUNCTURED stream of pattern pp
 // covering n stages; each chunk's punctured bytes are copied and expanded on
@@ -690,6 +743,42 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
     }
   }
 
+  // a previous call that failed half-way may have left staging in flight: settle it
+  for (int d = 0; d < nd; ++d) {
+    if (plan[d].empty()) continue;
+    DeviceGuard guard(devices[d]);
+    DevCtx& ctx = tl_ctx.devs[devices[d]];
+    for (int i = 0; i < 2; ++i) {
+      if (ctx.hout_pending[i] || ctx.hin_used[i]) {
+        cudaStreamSynchronize(ctx.st[i]);
+        ctx.hout_pending[i] = ctx.hin_used[i] = false;
+      }
+    }
+  }
+  const void* in_base = llr4 ? static_cast<const void*>(llr4) : static_cast<const void*>(llr);
+  const bool stage_in = !host_pinned(in_base), stage_out = !host_pinned(out_packed);
+  // H2D of one chunk (through the slot's pinned staging buffer when the caller's is pageable)
+  auto h2d = [&](DevCtx& ctx, int slot, cudaStream_t s, void* dst, const void* src, std::size_t bytes) -> vd_status {
+    if (!stage_in) {
+      VD_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "H2D chunk");
+      return VD_OK;
+    }
+    if (ctx.hin_used[slot]) VD_CUDA(cudaEventSynchronize(ctx.hin_free[slot]), "staging reuse");
+    if (vd_status st = ensure_host(&ctx.hin[slot], &ctx.hin_cap[slot], bytes)) return st;
+    if (!ctx.hin_free[slot]) VD_CUDA(cudaEventCreateWithFlags(&ctx.hin_free[slot], cudaEventDisableTiming), "event");
+    parallel_memcpy(ctx.hin[slot], src, bytes);
+    VD_CUDA(cudaMemcpyAsync(dst, ctx.hin[slot], bytes, cudaMemcpyHostToDevice, s), "H2D staged chunk");
+    VD_CUDA(cudaEventRecord(ctx.hin_free[slot], s), "event");
+    ctx.hin_used[slot] = true;
+    return VD_OK;
+  };
+  auto drain = [&](DevCtx& ctx, int slot) -> vd_status {  // staged output of the slot's previous chunk -> caller
+    if (!ctx.hout_pending[slot]) return VD_OK;
+    VD_CUDA(cudaEventSynchronize(ctx.hout_ready[slot]), "D2H staging");
+    parallel_memcpy(ctx.pend_dst[slot], ctx.hout[slot], ctx.pend_bytes[slot]);
+    ctx.hout_pending[slot] = false;
+    return VD_OK;
+  };
   // Issue: chunk i of every device on that device's stream i % 2. Within a
   // stream, the H2D of chunk i+2 is ordered after the kernel of chunk i.
   for (std::size_t i = 0; i < max_chunks; ++i) {
@@ -705,38 +794,51 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
       T* dl = static_cast<T*>(ctx.llr[slot]);
       if (pp) {
         const std::int64_t p0 = pp->off(wb), p1 = pp->off(we);
-        VD_CUDA(cudaMemcpyAsync(ctx.pun[slot], llr + p0, sizeof(T) * (p1 - p0), cudaMemcpyHostToDevice, s),
-                "H2D punctured chunk");
+        if (vd_status st = h2d(ctx, slot, s, ctx.pun[slot], llr + p0, sizeof(T) * (p1 - p0))) return st;
         if (vd_status st = launch_depuncture(*pp, static_cast<const std::int8_t*>(ctx.pun[slot]), wb, we - wb,
                                              reinterpret_cast<std::int8_t*>(dl), s))
           return st;
       } else if (llr4) {
         const std::int64_t e0 = wb * code->b, e1 = we * code->b;  // element range of the chunk
         const std::int64_t by0 = e0 >> 1, by1 = (e1 + 1) >> 1;
-        VD_CUDA(cudaMemcpyAsync(ctx.pun[slot], llr4 + by0, by1 - by0, cudaMemcpyHostToDevice, s), "H2D i4 chunk");
+        if (vd_status st = h2d(ctx, slot, s, ctx.pun[slot], llr4 + by0, by1 - by0)) return st;
         const cudaError_t eu = vd::launch_unpack_i4(static_cast<const std::uint8_t*>(ctx.pun[slot]),
                                                     static_cast<int>(e0 & 1), e1 - e0,
                                                     reinterpret_cast<std::int8_t*>(dl), s);
         if (eu != cudaSuccess) return cuda_fail(eu, "unpack i4 kernel");
       } else {
-        VD_CUDA(cudaMemcpyAsync(dl, llr + wb * code->b, sizeof(T) * (we - wb) * code->b, cudaMemcpyHostToDevice, s),
-                "H2D llr chunk");
+        if (vd_status st = h2d(ctx, slot, s, dl, llr + wb * code->b, sizeof(T) * (we - wb) * code->b)) return st;
       }
       const std::int64_t out_lo = c.f0 * cfg->f;  // multiple of 32 by construction
       const std::int64_t out_hi = std::min<std::int64_t>(c.f1 * cfg->f, n);
       vd_status st = decode_device<T>(code, cfg, n, dl, wb, c.f0, c.f1, ctx.out[slot], out_lo, nullptr, devices[d], s);
       if (st != VD_OK) return st;
       const std::int64_t words = (out_hi - out_lo + 31) / 32;
-      VD_CUDA(cudaMemcpyAsync(out_packed + out_lo / 32, ctx.out[slot], sizeof(std::uint32_t) * words,
-                              cudaMemcpyDeviceToHost, s),
-              "D2H packed bits");
+      const std::size_t obytes = sizeof(std::uint32_t) * words;
+      if (!stage_out) {
+        VD_CUDA(cudaMemcpyAsync(out_packed + out_lo / 32, ctx.out[slot], obytes, cudaMemcpyDeviceToHost, s),
+                "D2H packed bits");
+      } else {
+        if (vd_status st2 = drain(ctx, slot)) return st2;
+        if (vd_status st2 = ensure_host(&ctx.hout[slot], &ctx.hout_cap[slot], obytes)) return st2;
+        if (!ctx.hout_ready[slot]) VD_CUDA(cudaEventCreateWithFlags(&ctx.hout_ready[slot], cudaEventDisableTiming), "event");
+        VD_CUDA(cudaMemcpyAsync(ctx.hout[slot], ctx.out[slot], obytes, cudaMemcpyDeviceToHost, s), "D2H staged bits");
+        VD_CUDA(cudaEventRecord(ctx.hout_ready[slot], s), "event");
+        ctx.hout_pending[slot] = true;
+        ctx.pend_dst[slot] = out_packed + out_lo / 32;
+        ctx.pend_bytes[slot] = obytes;
+      }
     }
   }
   for (int d = 0; d < nd; ++d) {
     if (plan[d].empty()) continue;
     DeviceGuard guard(devices[d]);
     DevCtx& ctx = tl_ctx.devs[devices[d]];
-    for (int i = 0; i < 2; ++i) VD_CUDA(cudaStreamSynchronize(ctx.st[i]), "decode stream");
+    for (int i = 0; i < 2; ++i) {
+      if (vd_status st = drain(ctx, i)) return st;
+      VD_CUDA(cudaStreamSynchronize(ctx.st[i]), "decode stream");
+      ctx.hin_used[i] = false;
+    }
   }
   return VD_OK;
 }
