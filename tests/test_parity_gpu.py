@@ -385,3 +385,39 @@ def test_serial_decode_segment_parallel(code, port):
     exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2)
     packed, stats = vd.framed_decode_stream(q, n, t, cfg)
     assert np.array_equal(vd.unpack_bits(packed, n), exp)
+
+
+def test_concurrent_host_calls_pageable_and_pinned(port):
+    """The reference's BER sweep calls framed_decode from several host threads
+    at once (berlab.cpp:63-88): concurrent vd_decode_i8 calls (per-thread
+    streams and pinned staging of pageable buffers) all equal the oracle."""
+    import threading
+
+    import torch
+
+    t = trellis(*K7)
+    cfg = vd.FrameConfig(256, 20, 20)
+    jobs = []
+    for i in range(6):
+        n = 150_000 + 4099 * i
+        rx, _ = port.gen_bench_block(*K7, n, 2.0, 700 + i)
+        q = oracle.quantize(rx, 32.0)
+        if i % 2:
+            q = torch.from_numpy(q).pin_memory().numpy()  # pinned input for half the jobs
+        exp, _, _ = port.framed_decode(*K7, q, n, 256, 20, 20)
+        jobs.append((q, n, exp))
+    results = [None] * len(jobs)
+
+    def run(i):
+        q, n, _ = jobs[i]
+        for _ in range(3):
+            packed, _ = vd.framed_decode_stream(q, n, t, cfg, chunk_stages=1 << 15)
+            results[i] = vd.unpack_bits(packed, n)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(jobs))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for (q, n, exp), got in zip(jobs, results):
+        assert np.array_equal(got, exp)
