@@ -8,9 +8,10 @@
 //      the forward pass from the unit vector e_j (0 at j, -inf elsewhere)
 //      gives column j of the segment transfer matrix M_g (M_g[i][j] = best
 //      metric of a path j -> i through the segment). No decisions.
-//   B  boundary_kernel        one CTA, sequential over segments:
-//      sigma_{g+1} = M_g (x) sigma_g (64 x 64 max-plus mat-vec, int64; the
-//      next matrix is prefetched while the current one is reduced).
+//   B  boundary metrics sigma_g by a two-level max-plus scan: products of
+//      groups of 32 segment matrices (group_product_kernel, parallel), a
+//      sequential mat-vec chain over the group products, then each group's
+//      own chain from its start metrics in parallel (chain_matvec_kernel).
 //   C  segment_forward_kernel per segment (one warp each): the ordinary
 //      forward pass from the exact sigma_g, storing the decision words; the
 //      last segment also takes the argmax of the final metrics (lowest state
@@ -245,40 +246,61 @@ __global__ void __launch_bounds__(64) segment_matrix_cols_kernel(const SerialPar
   for (int i = 0; i < S; i += 4) *reinterpret_cast<int4*>(dst + i) = make_int4(sig[i], sig[i + 1], sig[i + 2], sig[i + 3]);
 }
 
+// Sequential max-plus chain sigma <- M_k (x) sigma over `count` matrices
+// (mats + k * S * S, column-major), writing the metrics BEFORE each step to
+// sig_out + k * S. CTA b handles chain b: mats += b * mat_stride, sig_out +=
+// b * out_stride, start vector sig_in + b * S (nullptr: zeros, decoder.cpp:109).
 // 256 threads: thread (q, i) = (tid >> 6, tid & 63) takes row i over the
-// columns j = q, q + 4, ...; the next segment's matrix is prefetched into
-// registers while the current one is reduced from shared memory.
-__global__ void __launch_bounds__(256) boundary_kernel(const SerialParams p) {
+// columns j = q, q + 4, ...; the next matrix is prefetched into registers
+// while the current one is reduced from shared memory.
+struct ChainArgs {
+  const std::int32_t* mats;
+  std::int64_t mat_stride;  // matrices per chain
+  const std::int64_t* sig_in;
+  std::int64_t* sig_out;
+  std::int64_t out_stride;  // S-vectors per chain
+  int total;                // matrices overall (the last chain may be shorter)
+  int per_chain;
+  int s;
+};
+
+__global__ void __launch_bounds__(256) chain_matvec_kernel(const ChainArgs a) {
   __shared__ std::int32_t m_s[2][64 * 64];
   __shared__ std::int64_t sig_s[64];
   __shared__ std::int64_t part[4][64];
   const int tid = threadIdx.x;
   const int i = tid & 63, q = tid >> 6;
-  const int S = p.s, SS = S * S;
+  const int S = a.s, SS = S * S;
+  const int b = blockIdx.x;
+  const int k0 = b * a.per_chain;
+  const int count = a.total - k0 < a.per_chain ? a.total - k0 : a.per_chain;
+  const std::int32_t* mats = a.mats + static_cast<std::int64_t>(b) * a.mat_stride * SS;
+  std::int64_t* out = a.sig_out + static_cast<std::int64_t>(b) * a.out_stride * S;
   constexpr int kPer = 64 * 64 / 256;  // matrix elements each thread moves
-  if (tid < 64) sig_s[tid] = 0;        // sigma_0 = 0 (decoder.cpp:109)
+  if (tid < 64) sig_s[tid] = (a.sig_in && tid < S) ? a.sig_in[static_cast<std::int64_t>(b) * S + tid] : 0;
   std::int32_t pre[kPer];
-  auto load = [&](int g) {
-    const std::int32_t* m = p.mat + static_cast<std::int64_t>(g) * SS;
+  auto load = [&](int k) {
+    const std::int32_t* m = mats + static_cast<std::int64_t>(k) * SS;
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) {
-      const int e = tid + 256 * k;
-      pre[k] = e < SS ? __ldg(m + e) : 0;
+    for (int e = 0; e < kPer; ++e) {
+      const int x = tid + 256 * e;
+      pre[e] = x < SS ? __ldg(m + x) : 0;
     }
   };
   auto stash = [&](int buf) {
 #pragma unroll
-    for (int k = 0; k < kPer; ++k) m_s[buf][tid + 256 * k] = pre[k];
+    for (int e = 0; e < kPer; ++e) m_s[buf][tid + 256 * e] = pre[e];
   };
+  if (count <= 0) return;
   load(0);
   stash(0);
   __syncthreads();
-  for (int g = 0; g < p.nseg; ++g) {
-    if (g + 1 < p.nseg) load(g + 1);  // in flight during this segment's reduction
-    if (tid < S) p.sig0[static_cast<std::int64_t>(g) * S + tid] = sig_s[tid];
+  for (int k = 0; k < count; ++k) {
+    if (k + 1 < count) load(k + 1);  // in flight during this step's reduction
+    if (tid < S) out[static_cast<std::int64_t>(k) * S + tid] = sig_s[tid];
     std::int64_t best = LLONG_MIN;
     if (i < S) {
-      const std::int32_t* m = m_s[g & 1];
+      const std::int32_t* m = m_s[k & 1];
       for (int j = q; j < S; j += 4) {
         const std::int64_t c = static_cast<std::int64_t>(m[j * S + i]) + sig_s[j];
         best = c > best ? c : best;
@@ -287,15 +309,77 @@ __global__ void __launch_bounds__(256) boundary_kernel(const SerialParams p) {
     part[q][i] = best;
     __syncthreads();
     if (tid < S) {
-      std::int64_t b = part[0][tid];
+      std::int64_t bb = part[0][tid];
 #pragma unroll
-      for (int k = 1; k < 4; ++k) b = part[k][tid] > b ? part[k][tid] : b;
-      sig_s[tid] = b;
+      for (int e = 1; e < 4; ++e) bb = part[e][tid] > bb ? part[e][tid] : bb;
+      sig_s[tid] = bb;
     }
-    if (g + 1 < p.nseg) stash((g + 1) & 1);
+    if (k + 1 < count) stash((k + 1) & 1);
     __syncthreads();
   }
-  if (tid < S) p.sig0[static_cast<std::int64_t>(p.nseg) * S + tid] = sig_s[tid];
+  if (tid < S) out[static_cast<std::int64_t>(count) * S + tid] = sig_s[tid];
+}
+
+// Group products P_b = M_{last} (x) ... (x) M_{first} of kGroup consecutive
+// segments (one CTA per group): P <- M_k (x) P, 64 x 64 x 64 max-plus per
+// step, register-tiled (each thread a 4 x 4 tile of P: per l one 16-byte
+// load of M's column and 4 loads of P's row, 16 add/max pairs). Entries stay
+// finite after >= K-1 stages; clamped at kNeg anyway. Matrices are padded to
+// 64 x 64 (unused rows / columns hold kNeg).
+constexpr int kGroup = 16;
+__global__ void __launch_bounds__(256) group_product_kernel(const SerialParams p, std::int32_t* prod) {
+  __shared__ __align__(16) std::int32_t P_s[64 * 64];
+  __shared__ __align__(16) std::int32_t M_s[64 * 64];
+  const int tid = threadIdx.x;
+  const int S = p.s, SS = S * S;
+  const int i0 = (tid & 15) * 4, j0 = (tid >> 4) * 4;  // tile rows i0..i0+3, cols j0..j0+3
+  const int g0 = blockIdx.x * kGroup;
+  const int count = p.nseg - g0 < kGroup ? p.nseg - g0 : kGroup;
+  auto load64 = [&](std::int32_t* dst, const std::int32_t* src) {  // S x S column-major -> 64 x 64
+    for (int x = tid; x < 64 * 64; x += 256) {
+      const int i = x & 63, j = x >> 6;
+      dst[x] = (i < S && j < S) ? __ldg(src + j * S + i) : kNeg;
+    }
+  };
+  load64(P_s, p.mat + static_cast<std::int64_t>(g0) * SS);
+  for (int k = 1; k < count; ++k) {
+    load64(M_s, p.mat + static_cast<std::int64_t>(g0 + k) * SS);
+    __syncthreads();
+    std::int32_t acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = kNeg;
+    }
+    for (int l = 0; l < 64; ++l) {
+      const int4 mcol = *reinterpret_cast<const int4*>(M_s + l * 64 + i0);  // M[i0..i0+3][l]
+      const std::int32_t m[4] = {mcol.x, mcol.y, mcol.z, mcol.w};
+      std::int32_t pr[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) pr[c] = P_s[(j0 + c) * 64 + l];  // P[l][j0 + c]
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const std::int32_t v = m[a] + pr[c];
+          acc[a][c] = v > acc[a][c] ? v : acc[a][c];
+        }
+      }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      *reinterpret_cast<int4*>(P_s + (j0 + c) * 64 + i0) =
+          make_int4(acc[0][c] > kNeg ? acc[0][c] : kNeg, acc[1][c] > kNeg ? acc[1][c] : kNeg,
+                    acc[2][c] > kNeg ? acc[2][c] : kNeg, acc[3][c] > kNeg ? acc[3][c] : kNeg);
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  for (int x = tid; x < SS; x += 256) {
+    const int i = x % S, j = x / S;
+    prod[static_cast<std::int64_t>(blockIdx.x) * SS + x] = P_s[j * 64 + i];
+  }
 }
 
 template <int NPL, int BT>
@@ -520,12 +604,30 @@ cudaError_t run(SerialParams p, cudaStream_t s) {
   p.endst = reinterpret_cast<std::int32_t*>(q);
   const std::int64_t warpsA = static_cast<std::int64_t>(p.nseg) * p.s;
   if (!launch_cols(p, s)) segment_matrix_kernel<NPL, BT><<<static_cast<unsigned>((warpsA + 3) / 4), 128, 0, s>>>(p);
-  boundary_kernel<<<1, 256, 0, s>>>(p);
+  // B: two-level max-plus scan of the segment matrices. Group products (in
+  // parallel), a sequential chain over the groups, then every group's own
+  // chain from its start metrics (in parallel).
+  const int ngroups = (p.nseg + kGroup - 1) / kGroup;
+  std::int32_t* prod = nullptr;
+  std::int64_t* gsig = nullptr;
+  if (cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&prod),
+                                      sizeof(std::int32_t) * S * S * ngroups + sizeof(std::int64_t) * S * (ngroups + 1), s);
+      e != cudaSuccess) {
+    cudaFreeAsync(buf, s);
+    return e;
+  }
+  gsig = reinterpret_cast<std::int64_t*>(prod + S * S * ngroups);
+  group_product_kernel<<<ngroups, 256, 0, s>>>(p, prod);
+  ChainArgs top{prod, 0, nullptr, gsig, 0, ngroups, ngroups, p.s};
+  chain_matvec_kernel<<<1, 256, 0, s>>>(top);
+  ChainArgs per{p.mat, kGroup, gsig, p.sig0, kGroup, p.nseg, kGroup, p.s};
+  chain_matvec_kernel<<<ngroups, 256, 0, s>>>(per);
   segment_forward_kernel<NPL, BT><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
   segment_map_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
   chain_kernel<<<1, 32, 0, s>>>(p);
   segment_emit_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
   cudaError_t e = cudaGetLastError();
+  cudaFreeAsync(prod, s);
   const cudaError_t ef = cudaFreeAsync(buf, s);
   return e != cudaSuccess ? e : ef;
 }
