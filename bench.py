@@ -48,6 +48,7 @@ WORKLOADS = {
     "C1": ((7, 2, [0o171, 0o133]), 1_000_000, "C1: K=7 r1/2 (171,133), 1M info bits, f=256 v1=20 v2=20"),
     "C3": ((7, 3, [0o133, 0o171, 0o165]), 1 << 26, "C3: K=7 r1/3 (133,171,165), 64 Mi info bits, f=256 v1=20 v2=20"),
     "C4": ((9, 2, [0o561, 0o753]), 1 << 28, "C4: K=9 r1/2 (561,753), 256 Mi info bits, f=256 v1=20 v2=20"),
+    "U3": ((9, 3, [0o557, 0o663, 0o711]), 1 << 28, "UMTS K=9 r1/3 (557,663,711), 256 Mi info bits, f=256 v1=20 v2=20"),
 }
 
 

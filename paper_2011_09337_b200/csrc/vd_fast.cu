@@ -1143,9 +1143,10 @@ using K9b = Code2<9, 0753, 0561>;
 using K5a = Code2<5, 023, 035>;
 using K6a = Code2<6, 053, 075>;
 using K8a = Code2<8, 0247, 0371>;
+using K9c = Code3<9, 0557, 0663, 0711>;  // UMTS / 3GPP rate 1/3
 using K7c = Code3<7, 0133, 0171, 0165>;  // LTE rate 1/3
 static_assert(K7a::sym() && K7b::sym() && K9a::sym() && K9b::sym() && K5a::sym() && K6a::sym() && K8a::sym() &&
-                  K7c::sym(),
+                  K7c::sym() && K9c::sym(),
               "fast-path codes must tap the newest and oldest register bits");
 
 constexpr int kMaxWarpsSmem = 8;   // smem-only survivor store
@@ -1461,6 +1462,7 @@ bool fast_path_supported(const DecodeLaunch& p) {
   if (p.b != 2 && p.b != 3) return false;
   Plan pl;
   if (K7c::matches(p.k, p.b, p.polys)) return plan<K7c, 16>(p, &pl);
+  if (K9c::matches(p.k, p.b, p.polys)) return plan<K9c, 16>(p, &pl);
   if (K7a::matches(p.k, p.b, p.polys)) return plan<K7a, 16>(p, &pl);
   if (K7b::matches(p.k, p.b, p.polys)) return plan<K7b, 16>(p, &pl);
   if (K9a::matches(p.k, p.b, p.polys)) return plan<K9a, 16>(p, &pl);
@@ -1476,6 +1478,7 @@ cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream) {
   cudaError_t err = cudaErrorNotSupported;
   if (try_variant<K7a, 16>(p, stream, &err)) return err;
   if (try_variant<K7c, 16>(p, stream, &err)) return err;
+  if (try_variant<K9c, 16>(p, stream, &err)) return err;
   if (try_variant<K7b, 16>(p, stream, &err)) return err;
   if (try_variant<K9a, 16>(p, stream, &err)) return err;
   if (try_variant<K9b, 16>(p, stream, &err)) return err;

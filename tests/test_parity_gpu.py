@@ -232,7 +232,7 @@ def test_error_behaviour_on_gpu():
 
 FAST_CODES = [(7, 2, [0o171, 0o133]), (7, 2, [0o133, 0o171]), (9, 2, [0o561, 0o753]), (9, 2, [0o753, 0o561]),
               (5, 2, [0o23, 0o35]), (6, 2, [0o53, 0o75]), (8, 2, [0o247, 0o371]),
-              (7, 3, [0o133, 0o171, 0o165])]
+              (7, 3, [0o133, 0o171, 0o165]), (9, 3, [0o557, 0o663, 0o711])]
 
 
 @pytest.mark.parametrize("code", FAST_CODES, ids=lambda c: f"K{c[0]}B{c[1]}_{c[2][0]:o}")
