@@ -277,44 +277,45 @@ __device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t 
   return d;
 }
 
+// Compile-time tuning knobs. The defaults are the measured-best settings;
+// the alternatives are kept so every row of profiles/r01_ab_notes.md can be
+// rebuilt with tools/build_variant.sh <name> -DVD_...=<value>.
 #ifndef VD_FMA_PAIRS
-#define VD_FMA_PAIRS 6
+#define VD_FMA_PAIRS 6      // butterflies per stage with FMA-pipe decision words (rest: ALU form)
 #endif
-// Butterflies per stage whose decision words use the FMA-pipe form (balances
-// the ALU and FMA pipes; the rest use the one-instruction ALU form).
 constexpr int kFmaPairs = VD_FMA_PAIRS;
+#ifndef VD_DEC_FORM
+#define VD_DEC_FORM 2       // FMA decision words: 2 = IADD3 d' + 2 IMAD(2 PT, d'); 1 = CN tables (-1 %)
+#endif
 #ifndef VD_PARAM_MULS
-#define VD_PARAM_MULS 0  // measured: 1 is 5 % slower (profiles/r01_ab_notes.md)
+#define VD_PARAM_MULS 0     // 1 = IMAD multipliers from the parameter bank (-5 %)
 #endif
 #ifndef VD_FMA_NEG
-#define VD_FMA_NEG 0
+#define VD_FMA_NEG 0        // 1 = table negations as IMADs (with VD_PARAM_MULS: -5 %)
 #endif
 #ifndef VD_MERGED_STORE
-#define VD_MERGED_STORE 0  // measured 0.6 % slower than separate TMEM / smem block copies
+#define VD_MERGED_STORE 0   // 1 = one straight-line block copy for TMEM and smem stores (-0.6 %)
 #endif
 #ifndef VD_LOCKSTEP
-#define VD_LOCKSTEP 1
+#define VD_LOCKSTEP 1       // 0 = persistent warps drift out of phase (-14 %)
 #endif
 #ifndef VD_FAST_TB
-#define VD_FAST_TB 1
+#define VD_FAST_TB 1        // serial-traceback fast path (+6 %)
 #endif
 #ifndef VD_GLOBAL_SPILL
-#define VD_GLOBAL_SPILL 2  // 1: spill to global rows only when no on-chip layout fits; 2: prefer 12 warps + spill
-#endif
-#ifndef VD_DEC_FORM
-#define VD_DEC_FORM 2  // measured +1 % over the CN-table form (profiles/r01_ab_notes.md)
+#define VD_GLOBAL_SPILL 2   // 2 = prefer 12 warps + global rows; 1 = only when no on-chip layout fits; 0 = never
 #endif
 #ifndef VD_PAD_HEAD
-#define VD_PAD_HEAD 1
+#define VD_PAD_HEAD 1       // head frames on the fast kernel via a zero-padded copy
 #endif
 #ifndef VD_RENORM_TABLE
-#define VD_RENORM_TABLE 1
+#define VD_RENORM_TABLE 1   // renormalisation folded into the next block's stage-0 tables
 #endif
 #ifndef VD_PF_SLACK
-#define VD_PF_SLACK 1
+#define VD_PF_SLACK 1       // unclamped LLR prefetch (callers keep kPfSlackStages of readable slack)
 #endif
 #ifndef VD_RENORM_EVERY
-#define VD_RENORM_EVERY 2
+#define VD_RENORM_EVERY 2   // blocks between renormalisations (2 or 4)
 #endif
 
 // (a & m) | (b & ~m) as one LOP3 that the compiler cannot re-associate into a
