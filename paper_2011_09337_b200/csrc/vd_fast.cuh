@@ -317,6 +317,15 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2   // blocks between renormalisations (2 or 4)
 #endif
+#ifndef VD_MAX_WARPS
+#define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
+#endif
+// Warps per CTA (launch bound). 16 = 4 per scheduler with part of the survivor
+// rows spilled to (L2-resident) global scratch: +3 % for K = 9, -3 % for K = 7.
+template <class C>
+constexpr int max_warps() {
+  return VD_MAX_WARPS ? VD_MAX_WARPS : (C::kK >= 9 ? 16 : 12);
+}
 
 // (a & m) | (b & ~m) as one LOP3 that the compiler cannot re-associate into a
 // serial chain (keeps the decision-compaction tree 3 deep).
@@ -585,7 +594,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
 }
 
 template <class C, int R, bool TM, bool GL>
-__global__ void __launch_bounds__(384, 1) fast_kernel(const FastParams fp) {
+__global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const FastParams fp) {
   using GEO = Geo<C, R>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, r = GEO::r, g = GEO::g;
   constexpr std::uint32_t BASE = 0x20002000u;  // offset-binary metric origin (8192 per half)
@@ -1290,7 +1299,14 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
     return kHeader + static_cast<std::size_t>(fp.smem_per_warp) * c.w <= static_cast<std::size_t>(kSmemMax);
   };
   bool ok = false;
-  if ((VD_GLOBAL_SPILL == 2 && warps_needed >= 12 * 148) || cap_rows >= 0) {
+  if (max_warps<C>() >= 16 && VD_GLOBAL_SPILL && warps_needed >= 16 * 148 && cap_rows < 0) {
+    // 16 warps per SM (4 per scheduler): TMEM + smem hold most rows, the rest
+    // spill to global scratch that stays L2-resident at this size
+    const Cand c16{16, 512};
+    ok = try_cand(c16, true);
+    if (ok) fp.warps_per_cta = 16;
+  }
+  if (!ok && ((VD_GLOBAL_SPILL == 2 && warps_needed >= 12 * 148) || cap_rows >= 0)) {
     ok = try_cand(cands[0], true);
     fp.warps_per_cta = 12;
   }
