@@ -395,32 +395,81 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
                         : std::strcmp(env_edges, "heads") == 0 ? 1 : std::strcmp(env_edges, "tails") == 0 ? 2 : 3;
   std::vector<std::int64_t> heads;
   std::map<int, std::vector<std::int64_t>> tails;  // v2' -> global frame ids
+  // BER-sweep batches repeat one block length: the per-block classification is
+  // memoised per length (valid for aligned blocks away from the stream end).
+  struct Memo {
+    std::int64_t len = -1, lo = 0, hi = 0;
+    std::vector<std::pair<std::int64_t, int>> edge;  // (m, kind): 0 generic, 1 head, 2 + v2' tail
+  } memo;
+  heads.reserve(static_cast<std::size_t>(nblocks));
+  std::vector<std::int64_t>* last_tail = nullptr;
+  int last_key = -1;
+  auto classify = [&](std::int32_t j, std::int64_t lo, std::int64_t hi, bool aligned,
+                      std::vector<std::pair<std::int64_t, int>>& outv) {
+    const std::int64_t nfj = bframe[j + 1] - bframe[j];
+    for (std::int64_t m = 0; m < nfj; ++m) {
+      if (m == lo && hi > lo) m = hi;  // skip the interior run (the fast kernel's)
+      if (m >= nfj) break;
+      int kind = 0;
+      if ((edge_mode & 1) && aligned && m < head_end && m * f + f + v2 <= lens[j]) {
+        kind = 1;
+      } else if ((edge_mode & 2) && aligned && one_tb && m >= head_end && m * f + f <= lens[j] &&
+                 m * f + f + v2 > lens[j] && f + v1 + (lens[j] - m * f - f) >= 16 &&
+                 bstage[j] + lens[j] + vd::kPfSlackStages <= n_total) {
+        kind = 2 + static_cast<int>(lens[j] - m * f - f);
+      }
+      outv.emplace_back(m, kind);
+    }
+  };
+  std::vector<std::pair<std::int64_t, int>> scratch_edges;
   for (std::int32_t j = 0; j < nblocks; ++j) {
+    const bool aligned = fast && (bstage[j] * B) % 4 == 0;
+    // memo valid: same length, aligned, and window + slack of every frame inside the stream
+    const bool regular = aligned && bstage[j] + lens[j] + L + vd::kPfSlackStages + f <= n_total;
     std::int64_t lo = 0, hi = 0;
-    if (fast && (bstage[j] * B) % 4 == 0) {
-      lo = (v1 + f - 1) / f;                                        // m*f >= v1
-      hi = lens[j] - f - v2 >= 0 ? (lens[j] - f - v2) / f + 1 : 0;  // m*f + f + v2 <= n_j
-      // window + the fast kernel's read slack inside the whole stream
-      const std::int64_t room = n_total - bstage[j] + v1 - L - vd::kPfSlackStages;
-      hi = std::min(hi, room >= 0 ? room / f + 1 : 0);
-      hi = std::max(hi, lo);
+    const std::vector<std::pair<std::int64_t, int>>* ev;
+    if (regular && memo.len == lens[j]) {
+      lo = memo.lo;
+      hi = memo.hi;
+      ev = &memo.edge;
+    } else {
+      if (aligned) {
+        lo = (v1 + f - 1) / f;                                        // m*f >= v1
+        hi = lens[j] - f - v2 >= 0 ? (lens[j] - f - v2) / f + 1 : 0;  // m*f + f + v2 <= n_j
+        // window + the fast kernel's read slack inside the whole stream
+        const std::int64_t room = n_total - bstage[j] + v1 - L - vd::kPfSlackStages;
+        hi = std::min(hi, room >= 0 ? room / f + 1 : 0);
+        hi = std::max(hi, lo);
+      }
+      scratch_edges.clear();
+      classify(j, lo, hi, aligned, scratch_edges);
+      if (regular) {
+        memo.len = lens[j];
+        memo.lo = lo;
+        memo.hi = hi;
+        memo.edge = scratch_edges;
+        ev = &memo.edge;
+      } else {
+        ev = &scratch_edges;
+      }
     }
     ilo[j] = static_cast<std::int32_t>(lo);
     ihi[j] = static_cast<std::int32_t>(hi);
     if (hi > lo && safe < 0) safe = bstage[j] + lo * f - v1;
     interior += hi - lo;
-    const std::int64_t nfj = bframe[j + 1] - bframe[j];
-    for (std::int64_t m = 0; m < nfj; ++m) {
-      if (m == lo && hi > lo) m = hi;  // skip the interior run (the fast kernel's)
-      if (m >= nfj) break;
-      const bool aligned = fast && (bstage[j] * B) % 4 == 0;
-      if ((edge_mode & 1) && aligned && m < head_end && m * f + f + v2 <= lens[j]) {
-        heads.push_back(bframe[j] + m);
-      } else if ((edge_mode & 2) && aligned && one_tb && m >= head_end && m * f + f <= lens[j] && m * f + f + v2 > lens[j] &&
-                 f + v1 + (lens[j] - m * f - f) >= 16 && bstage[j] + lens[j] + vd::kPfSlackStages <= n_total) {
-        tails[static_cast<int>(lens[j] - m * f - f)].push_back(bframe[j] + m);
+    for (const auto& e : *ev) {
+      const std::int64_t id = bframe[j] + e.first;
+      if (e.second == 0) {
+        edges.push_back(id);
+      } else if (e.second == 1) {
+        heads.push_back(id);
       } else {
-        edges.push_back(bframe[j] + m);
+        const int key = e.second - 2;
+        if (key != last_key) {
+          last_tail = &tails[key];
+          last_key = key;
+        }
+        last_tail->push_back(id);
       }
     }
   }
