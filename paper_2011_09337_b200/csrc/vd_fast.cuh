@@ -317,6 +317,10 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_RENORM_EVERY
 #define VD_RENORM_EVERY 2   // blocks between renormalisations (2 or 4)
 #endif
+#ifndef VD_TB_L2_PREFETCH
+#define VD_TB_L2_PREFETCH 1 // long-frame traceback: bulk L2 prefetch of the global rows ahead
+#endif
+constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -964,19 +968,19 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     // stage L-1 down to v1, output words aligned (f % 32 == 0). Per block:
     // one 4-word fetch, 4 x (funnel shift + bit select), 4 emitted bits into
     // a 32-bit accumulator stored with a plain 32-bit write every 8 blocks.
-    if (VD_FAST_TB && num_sub == 1 && (L & (LB - 1)) == 0 && (v1 & (LB - 1)) == 0 && (f & 31) == 0 &&
+    if (VD_FAST_TB && num_sub == 1 && ((L & (LB - 1)) == 0 || v2 >= LB) && (v1 & (LB - 1)) == 0 && (f & 31) == 0 &&
         __all_sync(kFull, ((obase + v1) & 31) == 0)) {
       std::uint32_t lp = P >> r;
       std::uint32_t u = (P & (R - 1)) | hsh;  // bit index into a decision word: register + 16 * half
       std::uint32_t acc32 = 0;
       std::uint32_t* const outw = p.out + ((obase + v1) >> 5);
       const int t_emit = v1 + f;  // blocks below this stage emit their 4 bits
-      auto step_block = [&](int tb0, const std::uint32_t (&wd)[LB]) {
+      auto step_block = [&](int tb0, const std::uint32_t (&wd)[LB], int jmax = 3 /* LB - 1 */) {
         const std::uint32_t rin = u & (R - 1);  // bit j = decoded bit of stage tb0 + j
 #pragma unroll
         for (int j = LB - 1; j >= 0; --j) {
           const std::uint32_t x = __funnelshift_r(wd[j], wd[j], u - static_cast<std::uint32_t>(j));  // bit u -> bit j
-          u = (x & (1u << j)) | (u & ~(1u << j));
+          if (j <= jmax) u = (x & (1u << j)) | (u & ~(1u << j));
         }
         if (tb0 < t_emit) {
           acc32 = (acc32 << LB) | rin;
@@ -987,16 +991,52 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         lp = pn >> r;
         u = (pn & (R - 1)) | hsh;
       };
-      int tb0 = L - LB;
+      int tb0 = (L - 1) & ~(LB - 1);
+      if ((L & (LB - 1)) != 0) {
+        // L % 4 != 0: the top block only walks phases 0 .. (L-1) % 4 (it lies in
+        // the v2 tail, v2 >= 4, so it emits nothing); peeled here, then whole blocks
+        const int jmax = (L - 1) & (LB - 1);
+        std::uint32_t wd[LB];
+        if (GL && tb0 >= t_gl) {
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = bc.grow_lane[(tb0 + j - t_gl) * 32 - lane + gcol + static_cast<int>(lp)];
+        } else if (!TM || tb0 >= t_split) {
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = dec[(tb0 + j - s_base) * 32 + gcol + lp];
+        } else {
+          std::uint32_t own[4];
+          tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
+        }
+        step_block(tb0, wd, jmax);
+        tb0 -= LB;
+      }
       if (GL && t_gl < L) {
         // global scratch rows: a group's G words of a stage are contiguous, so
-        // the loads do not depend on the traced lane and run one block ahead
+        // the loads do not depend on the traced lane and run one block ahead;
+        // the rows were written a whole forward pass ago (usually evicted to
+        // HBM), so lane 0 also pulls the next kTbL2Rows rows into L2 with one
+        // bulk prefetch every kTbL2Rows / 2 rows (rows are contiguous)
         const std::uint32_t* grow = bc.grow_lane - lane + gcol;
+        const unsigned char* grow_base = reinterpret_cast<const unsigned char*>(bc.grow_lane - lane);
+        auto l2_prefetch = [&](int tb) {  // rows [tb - kTbL2Rows, tb) below the current block
+          if (VD_TB_L2_PREFETCH && lane == 0) {
+            const int lo_row = max(tb - kTbL2Rows, t_gl) - t_gl, hi_row = tb - t_gl;
+            if (hi_row > lo_row) {
+              asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(grow_base + lo_row * 128),
+                           "r"(static_cast<unsigned>((hi_row - lo_row) * 128))
+                           : "memory");
+            }
+          }
+        };
+        l2_prefetch(tb0 + LB);  // the first window (the block at tb0 and the rows below it)
         if constexpr (G == 4) {
           uint4 cur[LB], nxt[LB];
 #pragma unroll
           for (int j = 0; j < LB; ++j) cur[j] = *reinterpret_cast<const uint4*>(grow + (tb0 + j - t_gl) * 32);
           for (; tb0 >= t_gl; tb0 -= LB) {
+            if (((tb0 - t_gl) & (kTbL2Rows / 2 - 1)) == 0) l2_prefetch(tb0 - kTbL2Rows / 2);
             if (tb0 - LB >= t_gl) {
 #pragma unroll
               for (int j = 0; j < LB; ++j)
@@ -1015,6 +1055,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
           }
         } else {
           for (; tb0 >= t_gl; tb0 -= LB) {
+            if (((tb0 - t_gl) & (kTbL2Rows / 2 - 1)) == 0) l2_prefetch(tb0 - kTbL2Rows / 2);
             std::uint32_t wd[LB];
 #pragma unroll
             for (int j = 0; j < LB; ++j) wd[j] = grow[(tb0 + j - t_gl) * 32 + lp];
