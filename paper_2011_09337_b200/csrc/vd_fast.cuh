@@ -302,6 +302,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_FAST_TB
 #define VD_FAST_TB 1        // serial-traceback fast path (+6 %)
 #endif
+#ifndef VD_FAST_SUB_TB
+#define VD_FAST_SUB_TB 1    // subframe (stored-max parallel) traceback fast path
+#endif
 #ifndef VD_GLOBAL_SPILL
 #define VD_GLOBAL_SPILL 2   // 2 = prefer 12 warps + global rows; 1 = only when no on-chip layout fits; 0 = never
 #endif
@@ -1077,6 +1080,56 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
 #pragma unroll
           for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
           step_block(tb0, wd);
+        }
+      }
+      continue;
+    }
+    // ---- subframe-traceback fast path (stored-max parallel traceback, e.g.
+    // f=320/20/45/32): every start stage has the same block phase, every
+    // subframe emits whole aligned words; one uniform block loop over the
+    // round, each lane walking only its own range (its top block partial).
+    if (VD_FAST_SUB_TB && num_sub > 1 && (step & 31) == 0 && (f % step) == 0 && (v1 & (LB - 1)) == 0 && v2 >= LB &&
+        __all_sync(kFull, !active || ((obase + sub_lo) & 31) == 0)) {
+      const int ph = (v1 + step + v2 - 1) & (LB - 1);  // phase of every start stage
+      const int stb = st_t & ~(LB - 1);                // this lane's top block
+      std::uint32_t lp = P >> r;
+      std::uint32_t u = (P & (R - 1)) | hsh;
+      std::uint32_t acc32 = 0;
+      std::uint32_t* const outw = p.out + ((obase + sub_lo) >> 5);
+      const int tstart = static_cast<int>(__reduce_max_sync(kFull, active ? static_cast<unsigned>(stb) : 0u));
+      const int tstop = static_cast<int>(__reduce_min_sync(kFull, active ? static_cast<unsigned>(sub_lo) : 0x7fffffffu));
+      for (int tb0 = tstart; tb0 >= tstop; tb0 -= LB) {
+        const bool act = active && tb0 <= stb && tb0 >= sub_lo;
+        const bool top = tb0 == stb;
+        std::uint32_t wd[LB];
+        if (TM && tb0 < t_split) {
+          std::uint32_t own[4];
+          tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
+        } else if (GL && tb0 >= t_gl) {
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = bc.grow_lane[(tb0 + j - t_gl) * 32 - lane + gcol + static_cast<int>(lp)];
+        } else {
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = dec[(tb0 + j - s_base) * 32 + gcol + lp];
+        }
+        const std::uint32_t rin = u & (R - 1);
+#pragma unroll
+        for (int j = LB - 1; j >= 0; --j) {
+          const std::uint32_t x = __funnelshift_r(wd[j], wd[j], u - static_cast<std::uint32_t>(j));
+          const bool walk = act && (j <= ph || !top);
+          if (walk) u = (x & (1u << j)) | (u & ~(1u << j));
+        }
+        if (act && tb0 < sub_hi) {
+          acc32 = (acc32 << LB) | rin;
+          if (((tb0 - sub_lo) & 31) == 0 && valid) outw[(tb0 - sub_lo) >> 5] = acc32;
+        }
+        if (act) {
+          const std::uint32_t pa = (lp << r) | (u & (R - 1));
+          const std::uint32_t pn = ((pa << r) | (pa >> (M - r))) & GEO::SMASK;  // undo the block relayout
+          lp = pn >> r;
+          u = (pn & (R - 1)) | hsh;
         }
       }
       continue;
