@@ -324,6 +324,9 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #define VD_TB_L2_PREFETCH 1 // long-frame traceback: bulk L2 prefetch of the global rows ahead
 #endif
 constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
+#ifndef VD_SMEM_DEFER
+#define VD_SMEM_DEFER 1     // smem-row blocks (MODE 1) buffer their 4 words and store after the block
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -576,7 +579,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       store_dec<TM, GL>(bc, tprev, word);
       tprev = t;
       rec(t, k);
-    } else if constexpr (MODE == 1) {
+    } else if constexpr (MODE == 1 && !VD_SMEM_DEFER) {
       bc.drow_lane[(t - 1 - bc.s_base) * 32] = word;
     } else if constexpr (MODE == 5) {
       bc.grow_lane[(t - 1 - bc.t_gl) * 32] = word;  // one coalesced 128-byte row per warp
@@ -585,6 +588,12 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     }
   }
   if constexpr (MODE == 2) tmem_st4(bc.taddr + static_cast<std::uint32_t>(blk * LB - 1 - bc.t_first), tw);
+  if constexpr (MODE == 1 && VD_SMEM_DEFER) {
+    // same register schedule as the TMEM blocks (an in-loop store per stage
+    // made ptxas rotate the metric registers with ~30 IMAD.MOVs per block)
+#pragma unroll
+    for (int k = 0; k < LB; ++k) bc.drow_lane[(blk * LB - 1 + k - bc.s_base) * 32] = tw[k];
+  }
   if constexpr (MODE == 4) {
     // merged straight-line block: the block's 4 words go to tensor memory or
     // to shared memory (one warp-uniform branch; one code copy for both halves
