@@ -253,6 +253,7 @@ struct FastParams {
   // constant-fold them, so the table / decision arithmetic written as
   // mad_u32 stays on the FMA pipe instead of becoming ALU-pipe LEA / IADD3.
   std::uint32_t one, two, m1;
+  std::uint32_t sh24;  // 1 << 24 (VD_TABLE_HI IMAD.HI multiplier)
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -327,6 +328,9 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_SMEM_DEFER
 #define VD_SMEM_DEFER 1     // smem-row blocks (MODE 1) buffer their 4 words and store after the block
 #endif
+#ifndef VD_TABLE_HI
+#define VD_TABLE_HI 0       // 1 = r1/2 tables as LOP3 masks + IMAD.HI shift-adds (FMA pipe)
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -380,7 +384,22 @@ struct FrameState {
   std::uint32_t one, two, m1;         // opaque 1, 2, -1 (IMAD multipliers)
   std::uint32_t two_p;                // 2 from the parameter bank (not constant-folded by ptxas)
   std::uint32_t corr;                 // pending renormalisation (BASE - ref per half), VD_RENORM_TABLE
+  std::uint32_t fwi[GEO::WPB][2];     // VD_TABLE_HI: fw interleaved like the LLR words (A | B halves)
+  std::uint32_t kc1n[GEO::LB];        // VD_TABLE_HI: kc[k][1] - 255 per half
+  std::uint32_t sh24, one_p;          // VD_TABLE_HI: 1 << 24 and 1 from the parameter bank
 };
+
+__device__ __forceinline__ std::uint32_t mad_hi_u32(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
+  std::uint32_t d;
+  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+  return d;
+}
+template <int LUT>
+__device__ __forceinline__ std::uint32_t lop3(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
+  std::uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
+  return r;
+}
 
 // Branch tables of one block: PT[k][x] = T_k[x ^ lane part] + 128 B per half
 // (T = the reference stage table, decoder.cpp:41-51, for frames A | B).
@@ -389,6 +408,25 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
   constexpr int LB = GEO::LB, B = GEO::B, WPB = GEO::WPB;
   constexpr std::uint32_t XM = C::kXM;
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * B) * 0x00010001u;
+  if constexpr (VD_TABLE_HI && B == 2) {
+    // Stage k's LLR pair of both frames sits in one interleaved raw word
+    // ilr = (A0, A1, B0, B1); with the lane's flips fwi (same interleave):
+    //   x0 = (ilr ^ fwi) & 0x00FF00FF, x1 << 8 = (ilr ^ fwi) & 0xFF00FF00,
+    //   (255 - x1) << 8 = ~(ilr ^ fwi) & 0xFF00FF00,
+    // and hi32(y * 2^24) = y >> 8 turns the shift-add into one IMAD.HI.
+#pragma unroll
+    for (int k = 0; k < LB; ++k) {
+      const int j = k >> 1, h = k & 1;
+      const std::uint32_t ilr = prmt(st.llr[BUF][0][j], st.llr[BUF][1][j], h ? 0x7632u : 0x5410u);
+      const std::uint32_t x0 = lop3<0x28>(ilr, st.fwi[j][h], 0x00ff00ffu);   // (a ^ b) & c
+      const std::uint32_t e1 = lop3<0x28>(ilr, st.fwi[j][h], 0xff00ff00u);
+      const std::uint32_t e1n = lop3<0x82>(ilr, st.fwi[j][h], 0xff00ff00u);  // ~(a ^ b) & c
+      PT[k][0] = mad_hi_u32(e1, st.sh24, mad_u32(x0, st.one_p, st.kc[k][0]));   // x0 + x1 + kc0
+      PT[k][1] = mad_hi_u32(e1n, st.sh24, mad_u32(x0, st.one_p, st.kc1n[k]));   // x0 - x1 + kc1
+#pragma unroll
+      for (int x = 0; x < GEO::NT; ++x) PT[k][x ^ XM] = OFFB - PT[k][x];
+    }
+  } else {
   // interleave frames A / B: lo = (A0, A1, B0, B1), hi = (A2, A3, B2, B3) of each word
   std::uint32_t il[WPB][2];
 #pragma unroll
@@ -423,6 +461,7 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
       // T[x ^ XM] = -T[x]
       PT[k][x ^ XM] = VD_FMA_NEG ? mad_u32(PT[k][x], st.m1, OFFB) : OFFB - PT[k][x];
     }
+  }
   }
 }
 
@@ -735,6 +774,15 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     }
 #pragma unroll
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
+#pragma unroll
+    for (int j = 0; j < WPB; ++j) {
+      st.fwi[j][0] = opaque(prmt(fw[j], fw[j], 0x5410u));
+      st.fwi[j][1] = opaque(prmt(fw[j], fw[j], 0x7632u));
+    }
+#pragma unroll
+    for (int k = 0; k < LB; ++k) st.kc1n[k] = opaque(st.kc[k][1] - 0x00ff00ffu);
+    st.sh24 = fp.sh24;
+    st.one_p = fp.one;
   }
   st.two_p = fp.two;
   st.corr = 0u;
@@ -1317,6 +1365,7 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   fp.one = 1u;
   fp.two = 2u;
   fp.m1 = 0xffffffffu;
+  fp.sh24 = 1u << 24;
   fp.L = p.f + p.v1 + p.v2;
   fp.nblk = (fp.L + GEO::LB - 1) / GEO::LB;
   fp.step = p.f0 > 0 ? p.f0 : p.f;
