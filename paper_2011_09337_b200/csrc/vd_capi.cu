@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <deque>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -688,21 +691,80 @@ bool host_pinned(const void* ptr) {
   return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
 }
 
+// Persistent host-copy workers (one pool per process, shared by every calling
+// thread): staging copies of pageable buffers are split over up to
+// VITDEC_COPY_THREADS threads (default: all hardware threads, at most 16)
+// without a thread create / join per chunk.
+class CopyPool {
+ public:
+  static CopyPool& get() {
+    static CopyPool* pool = new CopyPool();  // never destroyed: workers park on the condition variable at exit
+    return *pool;
+  }
+  int threads() const { return nt_; }
+  // Runs fn(0..parts-1): part 0 on the caller, the rest on the workers.
+  void run(int parts, const std::function<void(int)>& fn) {
+    struct Done {
+      std::mutex mu;
+      std::condition_variable cv;
+      int left;
+    } done;
+    done.left = parts - 1;
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      for (int i = 1; i < parts; ++i) {
+        q_.emplace_back([&fn, &done, i] {
+          fn(i);
+          std::lock_guard<std::mutex> dl(done.mu);
+          if (--done.left == 0) done.cv.notify_one();
+        });
+      }
+    }
+    cv_.notify_all();
+    fn(0);
+    std::unique_lock<std::mutex> dl(done.mu);
+    done.cv.wait(dl, [&] { return done.left == 0; });
+  }
+
+ private:
+  CopyPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    int nt = static_cast<int>(std::min(16u, hw));
+    if (const char* e = std::getenv("VITDEC_COPY_THREADS")) nt = std::max(1, std::atoi(e));
+    nt_ = nt;
+    for (int i = 1; i < nt; ++i) std::thread([this] { work(); }).detach();
+  }
+  void work() {
+    for (;;) {
+      std::function<void()> job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return !q_.empty(); });
+        job = std::move(q_.front());
+        q_.pop_front();
+      }
+      job();
+    }
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+  int nt_ = 1;
+};
+
 void parallel_memcpy(void* dst, const void* src, std::size_t bytes) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const std::size_t nt = bytes < (std::size_t{8} << 20) ? 1 : std::min<std::size_t>(8, std::max(1u, hw / 2));
+  constexpr std::size_t kMinPart = std::size_t{2} << 20;  // smaller copies: a pool hand-off costs more than it saves
+  CopyPool& pool = CopyPool::get();
+  const int nt = static_cast<int>(std::min<std::size_t>(pool.threads(), std::max<std::size_t>(1, bytes / kMinPart)));
   if (nt <= 1) {
     std::memcpy(dst, src, bytes);
     return;
   }
-  const std::size_t part = (bytes + nt - 1) / nt;
-  std::vector<std::thread> th;
-  for (std::size_t i = 1; i < nt; ++i) {
-    const std::size_t lo = i * part, len = lo < bytes ? std::min(part, bytes - lo) : 0;
-    if (len) th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, len); });
-  }
-  std::memcpy(dst, src, std::min(part, bytes));
-  for (auto& t : th) t.join();
+  const std::size_t part = (bytes / nt + 63) & ~std::size_t{63};
+  pool.run(nt, [=](int i) {
+    const std::size_t lo = static_cast<std::size_t>(i) * part;
+    if (lo < bytes) std::memcpy(static_cast<char*>(dst) + lo, static_cast<const char*>(src) + lo, std::min(part, bytes - lo));
+  });
 }
 
 vd_status ensure_host(void** p, std::size_t* cap, std::size_t bytes) {
