@@ -731,8 +731,15 @@ class CopyPool {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     int nt = static_cast<int>(std::min(16u, hw));
     if (const char* e = std::getenv("VITDEC_COPY_THREADS")) nt = std::max(1, std::atoi(e));
-    nt_ = nt;
-    for (int i = 1; i < nt; ++i) std::thread([this] { work(); }).detach();
+    nt_ = 1;
+    for (int i = 1; i < nt; ++i) {
+      try {
+        std::thread([this] { work(); }).detach();
+        ++nt_;
+      } catch (...) {  // no more threads: copy with the ones we have (never throw across the C-ABI)
+        break;
+      }
+    }
   }
   void work() {
     for (;;) {
