@@ -331,6 +331,9 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_TABLE_HI
 #define VD_TABLE_HI 0       // 1 = r1/2 tables as LOP3 masks + IMAD.HI shift-adds (FMA pipe)
 #endif
+#ifndef VD_RUNS
+#define VD_RUNS 1           // block loop as runs of one store mode (mode picked once per run, not per block)
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -980,10 +983,80 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     pfB += WPB;
     block_end(blk, buf_tag);
   };
+#if VD_RUNS && !VD_MERGED_STORE
+  // The store mode of a block (one_block's tests) only changes at a few block
+  // indices per frame: the end of the warm-up, the first / last clean block,
+  // the TMEM / smem / global-row splits, and the block holding the next
+  // stored-max start stage (which only moves inside a MODE 0 block). The loop
+  // picks the mode once per run of equal-mode blocks and runs them with a
+  // fixed body (same blocks, same modes, same order as one_block).
+  auto one_block_mode = [&](int blk, auto mode_tag, auto buf_tag) {
+    constexpr int MD = decltype(mode_tag)::value, BUF = decltype(buf_tag)::value;
+    run_block<C, GEO, MD, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
+    pf_off += WPB;
+    pfA += WPB;
+    pfB += WPB;
+    block_end(blk, buf_tag);
+  };
+  auto run_mode = [&](auto mode_tag, int& blk, int end) {
+    while (blk < end) {
+      if ((blk & 1) == 0) {
+        one_block_mode(blk, mode_tag, std::integral_constant<int, 0>{});
+        if (++blk >= end) break;
+      }
+      one_block_mode(blk, mode_tag, std::integral_constant<int, 1>{});
+      ++blk;
+    }
+  };
+  // first block index with blk * LB + LB - 2 >= x  /  with blk * LB - 1 >= x
+  auto first_hi = [](int x) { return (x + 1) / LB; };
+  auto first_lo = [](int x) { return (x + LB) / LB; };
+  const int nb_warm = v1 / LB;          // t0 + LB <= v1
+  const int cl_lo = first_lo(v1);       // t0 - 1 >= v1
+  const int cl_hi = first_hi(L);        // t0 + LB - 2 < L below this
+  const int tm_hi = first_hi(t_split);  // t0 + LB - 2 < t_split below this
+  const int sm_lo = first_lo(t_split);  // t0 - 1 >= t_split
+  const int gl_lo = first_lo(t_gl);     // t0 - 1 >= t_gl
+  const int sm_hi = GL ? min(first_hi(t_gl), cl_hi) : cl_hi;
+  int blk = 0;
+  while (blk < nblk) {
+    const int rb = next_rec / LB;  // block holding the next start stage
+    int md = 0, end = blk + 1;
+    if (blk < nb_warm) {
+      md = 3;
+      end = nb_warm;
+    } else if (blk >= cl_lo && blk < cl_hi && blk != rb) {
+      const int rend = rb > blk ? min(cl_hi, rb) : cl_hi;
+      if (GL && blk >= gl_lo) {
+        md = 5;
+        end = rend;
+      } else if (blk >= sm_lo && blk < sm_hi) {
+        md = 1;
+        end = min(rend, sm_hi);
+      } else if (TM && blk < tm_hi) {
+        md = 2;
+        end = min(rend, tm_hi);
+      }
+    }
+    if (md == 2) {
+      run_mode(std::integral_constant<int, 2>{}, blk, end);
+    } else if (md == 1) {
+      run_mode(std::integral_constant<int, 1>{}, blk, end);
+    } else if (md == 3) {
+      run_mode(std::integral_constant<int, 3>{}, blk, end);
+    } else if (GL && md == 5) {
+      run_mode(std::integral_constant<int, 5>{}, blk, end);
+    } else {
+      run_mode(std::integral_constant<int, 0>{}, blk, end);
+    }
+  }
+  (void)one_block;
+#else
   for (int blk = 0; blk < nblk; blk += 2) {
     one_block(blk, std::integral_constant<int, 0>{});
     if (blk + 1 < nblk) one_block(blk + 1, std::integral_constant<int, 1>{});
   }
+#endif
   // decisions of the last processed stage
   store_dec<TM, GL>(bc, tprev, compact16(st.wv[(nblk * LB - 1) & 1]));
   if constexpr (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
