@@ -623,7 +623,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       rec(t, k);
     } else if constexpr (MODE == 1 && !VD_SMEM_DEFER) {
       bc.drow_lane[(t - 1 - bc.s_base) * 32] = word;
-    } else if constexpr (MODE == 5) {
+    } else if constexpr (MODE == 5 && !VD_SMEM_DEFER) {
       bc.grow_lane[(t - 1 - bc.t_gl) * 32] = word;  // one coalesced 128-byte row per warp
     } else {
       tw[k] = word;  // one 4-column tensor-memory store per block, below
@@ -635,6 +635,12 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     // made ptxas rotate the metric registers with ~30 IMAD.MOVs per block)
 #pragma unroll
     for (int k = 0; k < LB; ++k) bc.drow_lane[(blk * LB - 1 + k - bc.s_base) * 32] = tw[k];
+  }
+  if constexpr (MODE == 5 && VD_SMEM_DEFER) {
+    // global rows: one address per block, coalesced 128-byte rows per warp
+    std::uint32_t* const gp = bc.grow_lane + static_cast<std::ptrdiff_t>(blk * LB - 1 - bc.t_gl) * 32;
+#pragma unroll
+    for (int k = 0; k < LB; ++k) gp[k * 32] = tw[k];
   }
   if constexpr (MODE == 4) {
     // merged straight-line block: the block's 4 words go to tensor memory or
