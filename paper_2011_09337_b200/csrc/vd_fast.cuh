@@ -334,6 +334,9 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_RUNS
 #define VD_RUNS 1           // block loop as runs of one store mode (mode picked once per run, not per block)
 #endif
+#ifndef VD_EDGE_MODES
+#define VD_EDGE_MODES 0     // 1 = straight-line blocks for the first decision block and the TMEM/smem split block (A/B: C3 +1.6 %, C5 -0.1 %, f0=32 -0.9 %)
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -630,6 +633,27 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     }
   }
   if constexpr (MODE == 2) tmem_st4(bc.taddr + static_cast<std::uint32_t>(blk * LB - 1 - bc.t_first), tw);
+  if constexpr (MODE == 6) {
+    // TMEM/smem split block (t0 == t_split): the pending stage t0 - 1 is the
+    // last TMEM column, stages t0 .. t0 + LB - 2 the first smem rows
+    tmem_st1(bc.taddr + static_cast<std::uint32_t>(blk * LB - 1 - bc.t_first), tw[0]);
+#pragma unroll
+    for (int k = 1; k < LB; ++k) bc.drow_lane[(blk * LB - 1 + k - bc.s_base) * 32] = tw[k];
+  }
+  if constexpr (MODE == 7) {
+    // first decision block (t0 <= v1 < t0 + LB): stages below v1 have no slot
+#pragma unroll
+    for (int k = 0; k < LB; ++k) {
+      const int tp = blk * LB - 1 + k;
+      if (tp >= bc.v1) {
+        if (TM) {
+          tmem_st1(bc.taddr + static_cast<std::uint32_t>(tp - bc.t_first), tw[k]);
+        } else {
+          bc.drow_lane[(tp - bc.s_base) * 32] = tw[k];
+        }
+      }
+    }
+  }
   if constexpr (MODE == 1 && VD_SMEM_DEFER) {
     // same register schedule as the TMEM blocks (an in-loop store per stage
     // made ptxas rotate the metric registers with ~30 IMAD.MOVs per block)
@@ -1031,6 +1055,12 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     if (blk < nb_warm) {
       md = 3;
       end = nb_warm;
+    } else if (VD_EDGE_MODES && blk < cl_lo && blk < cl_hi && blk != rb &&
+               (TM ? blk * LB + LB - 2 < t_split : (!GL || blk * LB + LB - 2 < t_gl))) {
+      md = 7;  // the one block with t0 <= v1 < t0 + LB
+    } else if (VD_EDGE_MODES && TM && blk * LB == t_split && blk >= cl_lo && blk < cl_hi && blk != rb &&
+               (!GL || blk * LB + LB - 2 < t_gl)) {
+      md = 6;
     } else if (blk >= cl_lo && blk < cl_hi && blk != rb) {
       const int rend = rb > blk ? min(cl_hi, rb) : cl_hi;
       if (GL && blk >= gl_lo) {
@@ -1052,6 +1082,10 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       run_mode(std::integral_constant<int, 3>{}, blk, end);
     } else if (GL && md == 5) {
       run_mode(std::integral_constant<int, 5>{}, blk, end);
+    } else if (VD_EDGE_MODES && md == 7) {
+      run_mode(std::integral_constant<int, 7>{}, blk, end);
+    } else if (VD_EDGE_MODES && TM && md == 6) {
+      run_mode(std::integral_constant<int, 6>{}, blk, end);
     } else {
       run_mode(std::integral_constant<int, 0>{}, blk, end);
     }
