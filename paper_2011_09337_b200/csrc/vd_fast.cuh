@@ -337,6 +337,12 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_EDGE_MODES
 #define VD_EDGE_MODES 0     // 1 = straight-line blocks for the first decision block and the TMEM/smem split block (A/B: C3 +1.6 %, C5 -0.1 %, f0=32 -0.9 %)
 #endif
+#ifndef VD_TB_TMEM_PIPE
+#define VD_TB_TMEM_PIPE 0   // 1 = serial traceback: tensor-memory block loads issued one block ahead (-1.1 %)
+#endif
+#ifndef VD_TB_SMEM_PIPE
+#define VD_TB_SMEM_PIPE 0   // 1 = serial traceback: smem rows as 16-byte group loads one block ahead, G = 4 (-0.6 % more)
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -486,6 +492,18 @@ __device__ __forceinline__ void tmem_ld4(std::uint32_t taddr, std::uint32_t (&v)
                : "r"(taddr)
                : "memory");
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Split form of tmem_ld4: the load, and a wait that names the destination
+// registers (so no use of them can be scheduled before the wait).
+__device__ __forceinline__ void tmem_ld4_async(std::uint32_t taddr, std::uint32_t (&v)[4]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+               : "r"(taddr)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_ld(std::uint32_t (&v)[4]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])::"memory");
 }
 
 struct BlockCtx {
@@ -1236,14 +1254,67 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
           }
         }
       }
-      for (; tb0 >= v1 && (!TM || tb0 >= t_split); tb0 -= LB) {  // shared-memory rows
-        std::uint32_t wd[LB];
-        const std::uint32_t* src = dec + (tb0 - s_base) * 32 + gcol + lp;
+      bool smem_done = false;
+#if VD_TB_SMEM_PIPE
+      if constexpr (G == 4) {
+        // shared-memory rows, one block ahead: the group's 4 words of a stage
+        // are one 16-byte load that does not depend on the traced lane
+        smem_done = true;
+        if (tb0 >= v1 && (!TM || tb0 >= t_split)) {
+          const std::uint32_t* grp_row = dec + gcol - s_base * 32;
+          uint4 cur[LB];
 #pragma unroll
-        for (int j = 0; j < LB; ++j) wd[j] = src[j * 32];
-        step_block(tb0, wd);
+          for (int j = 0; j < LB; ++j) cur[j] = *reinterpret_cast<const uint4*>(grp_row + (tb0 + j) * 32);
+          for (; tb0 >= v1 && (!TM || tb0 >= t_split); tb0 -= LB) {
+            uint4 nxt[LB];
+            const bool more = tb0 - LB >= v1 && (!TM || tb0 - LB >= t_split);
+#pragma unroll
+            for (int j = 0; j < LB; ++j)
+              nxt[j] = more ? *reinterpret_cast<const uint4*>(grp_row + (tb0 - LB + j) * 32) : cur[j];
+            std::uint32_t wd[LB];
+#pragma unroll
+            for (int j = 0; j < LB; ++j) {
+              const uint4 c = cur[j];
+              const std::uint32_t lo = (lp & 1u) ? c.y : c.x, hi = (lp & 1u) ? c.w : c.z;
+              wd[j] = (lp & 2u) ? hi : lo;
+            }
+            step_block(tb0, wd);
+#pragma unroll
+            for (int j = 0; j < LB; ++j) cur[j] = nxt[j];
+          }
+        }
+      }
+#endif
+      if (!smem_done) {
+        for (; tb0 >= v1 && (!TM || tb0 >= t_split); tb0 -= LB) {  // shared-memory rows
+          std::uint32_t wd[LB];
+          const std::uint32_t* src = dec + (tb0 - s_base) * 32 + gcol + lp;
+#pragma unroll
+          for (int j = 0; j < LB; ++j) wd[j] = src[j * 32];
+          step_block(tb0, wd);
+        }
       }
       if constexpr (TM) {
+#if VD_TB_TMEM_PIPE
+        // tensor-memory columns, one block ahead: the 4-column load of the
+        // next block does not depend on the traced state, so it is issued
+        // before this block's shuffles / steps and waited for after them
+        if (tb0 >= v1) {
+          std::uint32_t own[4];
+          tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
+          for (; tb0 >= v1; tb0 -= LB) {
+            std::uint32_t nxt[4] = {0u, 0u, 0u, 0u}, wd[LB];
+            const bool more = tb0 - LB >= v1;
+            if (more) tmem_ld4_async(bc.taddr + static_cast<std::uint32_t>(tb0 - LB - t_first), nxt);
+#pragma unroll
+            for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
+            step_block(tb0, wd);
+            if (more) tmem_wait_ld(nxt);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) own[j] = nxt[j];
+          }
+        }
+#else
         for (; tb0 >= v1; tb0 -= LB) {  // tensor-memory columns
           std::uint32_t own[4], wd[LB];
           tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
@@ -1251,6 +1322,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
           for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
           step_block(tb0, wd);
         }
+#endif
       }
       continue;
     }
