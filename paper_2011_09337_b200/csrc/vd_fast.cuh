@@ -343,6 +343,9 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_TB_SMEM_PIPE
 #define VD_TB_SMEM_PIPE 0   // 1 = serial traceback: smem rows as 16-byte group loads one block ahead, G = 4 (-0.6 % more)
 #endif
+#ifndef VD_TB_WP
+#define VD_TB_WP 1          // serial traceback: output words through a running pointer
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -1166,6 +1169,8 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       std::uint32_t acc32 = 0;
       std::uint32_t* const outw = p.out + ((obase + v1) >> 5);
       const int t_emit = v1 + f;  // blocks below this stage emit their 4 bits
+      std::uint32_t* wp = outw + ((t_emit - LB - v1) >> 5);  // word of the first emitting block
+      (void)wp;
       auto step_block = [&](int tb0, const std::uint32_t (&wd)[LB], int jmax = 3 /* LB - 1 */) {
         const std::uint32_t rin = u & (R - 1);  // bit j = decoded bit of stage tb0 + j
 #pragma unroll
@@ -1175,7 +1180,15 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         }
         if (tb0 < t_emit) {
           acc32 = (acc32 << LB) | rin;
+#if VD_TB_WP
+          // running word pointer (one decrement per store, no address math per block)
+          if (((tb0 - v1) & 31) == 0) {
+            if (valid) *wp = acc32;
+            --wp;
+          }
+#else
           if (((tb0 - v1) & 31) == 0 && valid) outw[(tb0 - v1) >> 5] = acc32;
+#endif
         }
         const std::uint32_t pa = (lp << r) | (u & (R - 1));
         const std::uint32_t pn = ((pa << r) | (pa >> (M - r))) & GEO::SMASK;  // undo the block relayout
