@@ -1351,6 +1351,8 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       std::uint32_t u = (P & (R - 1)) | hsh;
       std::uint32_t acc32 = 0;
       std::uint32_t* const outw = p.out + ((obase + sub_lo) >> 5);
+      std::uint32_t* wp = outw + ((sub_hi - LB - sub_lo) >> 5);  // word of this lane's first emitting block
+      (void)wp;
       const int tstart = static_cast<int>(__reduce_max_sync(kFull, active ? static_cast<unsigned>(stb) : 0u));
       const int tstop = static_cast<int>(__reduce_min_sync(kFull, active ? static_cast<unsigned>(sub_lo) : 0x7fffffffu));
       for (int tb0 = tstart; tb0 >= tstop; tb0 -= LB) {
@@ -1378,7 +1380,14 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         }
         if (act && tb0 < sub_hi) {
           acc32 = (acc32 << LB) | rin;
+#if VD_TB_WP
+          if (((tb0 - sub_lo) & 31) == 0) {
+            if (valid) *wp = acc32;
+            --wp;
+          }
+#else
           if (((tb0 - sub_lo) & 31) == 0 && valid) outw[(tb0 - sub_lo) >> 5] = acc32;
+#endif
         }
         if (act) {
           const std::uint32_t pa = (lp << r) | (u & (R - 1));
