@@ -346,6 +346,9 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_TB_WP
 #define VD_TB_WP 1          // serial traceback: output words through a running pointer
 #endif
+#ifndef VD_TB_BITSEL
+#define VD_TB_BITSEL 1      // traceback steps: bit j of the rotated word merged with one LOP3
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -362,6 +365,13 @@ template <std::uint32_t MASK>
 __device__ __forceinline__ std::uint32_t bitsel(std::uint32_t a, std::uint32_t b) {
   std::uint32_t r;
   asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(MASK));  // 0xE4: c ? a : b
+  return r;
+}
+
+// (a & m) | (b & ~m) as one LOP3 (m a compile-time constant after unrolling)
+__device__ __forceinline__ std::uint32_t bitsel_m(std::uint32_t a, std::uint32_t b, std::uint32_t m) {
+  std::uint32_t r;
+  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "r"(m));
   return r;
 }
 
@@ -1176,7 +1186,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
 #pragma unroll
         for (int j = LB - 1; j >= 0; --j) {
           const std::uint32_t x = __funnelshift_r(wd[j], wd[j], u - static_cast<std::uint32_t>(j));  // bit u -> bit j
-          if (j <= jmax) u = (x & (1u << j)) | (u & ~(1u << j));
+          if (j <= jmax) u = VD_TB_BITSEL ? bitsel_m(x, u, 1u << j) : (x & (1u << j)) | (u & ~(1u << j));
         }
         if (tb0 < t_emit) {
           acc32 = (acc32 << LB) | rin;
@@ -1376,7 +1386,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         for (int j = LB - 1; j >= 0; --j) {
           const std::uint32_t x = __funnelshift_r(wd[j], wd[j], u - static_cast<std::uint32_t>(j));
           const bool walk = act && (j <= ph || !top);
-          if (walk) u = (x & (1u << j)) | (u & ~(1u << j));
+          if (walk) u = VD_TB_BITSEL ? bitsel_m(x, u, 1u << j) : (x & (1u << j)) | (u & ~(1u << j));
         }
         if (act && tb0 < sub_hi) {
           acc32 = (acc32 << LB) | rin;
