@@ -349,6 +349,9 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #ifndef VD_TB_BITSEL
 #define VD_TB_BITSEL 1      // traceback steps: bit j of the rotated word merged with one LOP3
 #endif
+#ifndef VD_RUN_LOOP1
+#define VD_RUN_LOOP1 0      // 1 = one block per run-loop iteration, body picked by parity
+#endif
 #ifndef VD_MAX_WARPS
 #define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
 #endif
@@ -1060,6 +1063,15 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     block_end(blk, buf_tag);
   };
   auto run_mode = [&](auto mode_tag, int& blk, int end) {
+#if VD_RUN_LOOP1
+    for (; blk < end; ++blk) {  // one block per iteration, body by parity (no loop break)
+      if ((blk & 1) == 0) {
+        one_block_mode(blk, mode_tag, std::integral_constant<int, 0>{});
+      } else {
+        one_block_mode(blk, mode_tag, std::integral_constant<int, 1>{});
+      }
+    }
+#else
     while (blk < end) {
       if ((blk & 1) == 0) {
         one_block_mode(blk, mode_tag, std::integral_constant<int, 0>{});
@@ -1068,6 +1080,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       one_block_mode(blk, mode_tag, std::integral_constant<int, 1>{});
       ++blk;
     }
+#endif
   };
   // first block index with blk * LB + LB - 2 >= x  /  with blk * LB - 1 >= x
   auto first_hi = [](int x) { return (x + 1) / LB; };
