@@ -353,10 +353,12 @@ constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
 #define VD_RUN_LOOP1 0      // 1 = one block per run-loop iteration, body picked by parity
 #endif
 #ifndef VD_MAX_WARPS
-#define VD_MAX_WARPS 0      // 0: per code (16 for K >= 9, else 12); 12 / 16: force
+#define VD_MAX_WARPS 12     // warps per CTA: 12 (16 = 4 per scheduler with L2-resident spill rows: C5 -5 %, C4 -4 % after the run-loop / traceback changes)
 #endif
 // Warps per CTA (launch bound). 16 = 4 per scheduler with part of the survivor
-// rows spilled to (L2-resident) global scratch: +3 % for K = 9, -3 % for K = 7.
+// rows spilled to (L2-resident) global scratch was +3 % for K = 9 before the
+// block loop ran in mode runs; since then 12 is faster for every code
+// (C4 27.8 -> 29.0 Gbps, profiles/r01_ab_notes.md). 0 = per code (16 for K >= 9).
 template <class C>
 constexpr int max_warps() {
   return VD_MAX_WARPS ? VD_MAX_WARPS : (C::kK >= 9 ? 16 : 12);
