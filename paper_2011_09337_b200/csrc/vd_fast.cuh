@@ -249,11 +249,10 @@ struct FastParams {
   std::int64_t head_pitch;  // stages per block in llr_head (batched: v1 + head window)
   int tm_alloc;  // TMEM columns allocated per CTA (power of two)
   std::int64_t safe_stage;  // window start of an interior frame (loads of empty frame slots)
-  // IMAD multipliers 1, 2, -1 read from the parameter bank: ptxas cannot
-  // constant-fold them, so the table / decision arithmetic written as
-  // mad_u32 stays on the FMA pipe instead of becoming ALU-pipe LEA / IADD3.
-  std::uint32_t one, two, m1;
-  std::uint32_t sh24;  // 1 << 24 (VD_TABLE_HI IMAD.HI multiplier)
+  // IMAD multiplier 2 read from the parameter bank: ptxas cannot constant-fold
+  // it, so the decision arithmetic written as mad_u32 stays on the FMA pipe
+  // instead of becoming ALU-pipe LEA / IADD3.
+  std::uint32_t two;
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -278,28 +277,13 @@ __device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t 
   return d;
 }
 
-// Compile-time tuning knobs. The defaults are the measured-best settings;
-// the alternatives are kept so every row of profiles/r01_ab_notes.md can be
-// rebuilt with tools/build_variant.sh <name> -DVD_...=<value>.
+// Compile-time tuning knobs (the defaults are the measured-best settings;
+// every rejected alternative is logged in profiles/r01_ab_notes.md /
+// profiles/r02_ab_notes.md and was removed from the source).
 #ifndef VD_FMA_PAIRS
 #define VD_FMA_PAIRS 6      // butterflies per stage with FMA-pipe decision words (rest: ALU form)
 #endif
 constexpr int kFmaPairs = VD_FMA_PAIRS;
-#ifndef VD_DEC_FORM
-#define VD_DEC_FORM 2       // FMA decision words: 2 = IADD3 d' + 2 IMAD(2 PT, d'); 1 = CN tables (-1 %)
-#endif
-#ifndef VD_PARAM_MULS
-#define VD_PARAM_MULS 0     // 1 = IMAD multipliers from the parameter bank (-5 %)
-#endif
-#ifndef VD_FMA_NEG
-#define VD_FMA_NEG 0        // 1 = table negations as IMADs (with VD_PARAM_MULS: -5 %)
-#endif
-#ifndef VD_MERGED_STORE
-#define VD_MERGED_STORE 0   // 1 = one straight-line block copy for TMEM and smem stores (-0.6 %)
-#endif
-#ifndef VD_LOCKSTEP
-#define VD_LOCKSTEP 1       // 0 = persistent warps drift out of phase (-14 %)
-#endif
 #ifndef VD_FAST_TB
 #define VD_FAST_TB 1        // serial-traceback fast path (+6 %)
 #endif
@@ -312,48 +296,12 @@ constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_PAD_HEAD
 #define VD_PAD_HEAD 1       // head frames on the fast kernel via a zero-padded copy
 #endif
-#ifndef VD_RENORM_TABLE
-#define VD_RENORM_TABLE 1   // renormalisation folded into the next block's stage-0 tables
-#endif
-#ifndef VD_PF_SLACK
-#define VD_PF_SLACK 1       // unclamped LLR prefetch (callers keep kPfSlackStages of readable slack)
-#endif
-#ifndef VD_RENORM_EVERY
-#define VD_RENORM_EVERY 2   // blocks between renormalisations (2 or 4)
-#endif
 #ifndef VD_TB_L2_PREFETCH
 #define VD_TB_L2_PREFETCH 1 // long-frame traceback: bulk L2 prefetch of the global rows ahead
 #endif
 constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
-#ifndef VD_SMEM_DEFER
-#define VD_SMEM_DEFER 1     // smem-row blocks (MODE 1) buffer their 4 words and store after the block
-#endif
-#ifndef VD_TABLE_HI
-#define VD_TABLE_HI 0       // 1 = r1/2 tables as LOP3 masks + IMAD.HI shift-adds (FMA pipe)
-#endif
-#ifndef VD_RUNS
-#define VD_RUNS 1           // block loop as runs of one store mode (mode picked once per run, not per block)
-#endif
-#ifndef VD_EDGE_MODES
-#define VD_EDGE_MODES 0     // 1 = straight-line blocks for the first decision block and the TMEM/smem split block (A/B: C3 +1.6 %, C5 -0.1 %, f0=32 -0.9 %)
-#endif
-#ifndef VD_TB_TMEM_PIPE
-#define VD_TB_TMEM_PIPE 0   // 1 = serial traceback: tensor-memory block loads issued one block ahead (-1.1 %)
-#endif
-#ifndef VD_TB_SMEM_PIPE
-#define VD_TB_SMEM_PIPE 0   // 1 = serial traceback: smem rows as 16-byte group loads one block ahead, G = 4 (-0.6 % more)
-#endif
-#ifndef VD_TB_WP
-#define VD_TB_WP 1          // serial traceback: output words through a running pointer
-#endif
-#ifndef VD_TB_BITSEL
-#define VD_TB_BITSEL 1      // traceback steps: bit j of the rotated word merged with one LOP3
-#endif
-#ifndef VD_RUN_LOOP1
-#define VD_RUN_LOOP1 0      // 1 = one block per run-loop iteration, body picked by parity
-#endif
 #ifndef VD_MAX_WARPS
-#define VD_MAX_WARPS 12     // warps per CTA: 12 (16 = 4 per scheduler with L2-resident spill rows: C5 -5 %, C4 -4 % after the run-loop / traceback changes)
+#define VD_MAX_WARPS 12     // warps per CTA: 12 (16 = 4 per scheduler with L2-resident spill rows: C5 -5 %, C4 -4 %)
 #endif
 // Warps per CTA (launch bound). 16 = 4 per scheduler with part of the survivor
 // rows spilled to (L2-resident) global scratch was +3 % for K = 9 before the
@@ -411,25 +359,9 @@ struct FrameState {
   std::uint32_t fw[GEO::WPB];
   std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : 3];
   std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
-  std::uint32_t one, two, m1;         // opaque 1, 2, -1 (IMAD multipliers)
   std::uint32_t two_p;                // 2 from the parameter bank (not constant-folded by ptxas)
-  std::uint32_t corr;                 // pending renormalisation (BASE - ref per half), VD_RENORM_TABLE
-  std::uint32_t fwi[GEO::WPB][2];     // VD_TABLE_HI: fw interleaved like the LLR words (A | B halves)
-  std::uint32_t kc1n[GEO::LB];        // VD_TABLE_HI: kc[k][1] - 255 per half
-  std::uint32_t sh24, one_p;          // VD_TABLE_HI: 1 << 24 and 1 from the parameter bank
+  std::uint32_t corr;                 // pending renormalisation (BASE - ref per half)
 };
-
-__device__ __forceinline__ std::uint32_t mad_hi_u32(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
-  std::uint32_t d;
-  asm("mad.hi.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
-  return d;
-}
-template <int LUT>
-__device__ __forceinline__ std::uint32_t lop3(std::uint32_t a, std::uint32_t b, std::uint32_t c) {
-  std::uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, %4;" : "=r"(r) : "r"(a), "r"(b), "r"(c), "n"(LUT));
-  return r;
-}
 
 // Branch tables of one block: PT[k][x] = T_k[x ^ lane part] + 128 B per half
 // (T = the reference stage table, decoder.cpp:41-51, for frames A | B).
@@ -438,25 +370,6 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
   constexpr int LB = GEO::LB, B = GEO::B, WPB = GEO::WPB;
   constexpr std::uint32_t XM = C::kXM;
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * B) * 0x00010001u;
-  if constexpr (VD_TABLE_HI && B == 2) {
-    // Stage k's LLR pair of both frames sits in one interleaved raw word
-    // ilr = (A0, A1, B0, B1); with the lane's flips fwi (same interleave):
-    //   x0 = (ilr ^ fwi) & 0x00FF00FF, x1 << 8 = (ilr ^ fwi) & 0xFF00FF00,
-    //   (255 - x1) << 8 = ~(ilr ^ fwi) & 0xFF00FF00,
-    // and hi32(y * 2^24) = y >> 8 turns the shift-add into one IMAD.HI.
-#pragma unroll
-    for (int k = 0; k < LB; ++k) {
-      const int j = k >> 1, h = k & 1;
-      const std::uint32_t ilr = prmt(st.llr[BUF][0][j], st.llr[BUF][1][j], h ? 0x7632u : 0x5410u);
-      const std::uint32_t x0 = lop3<0x28>(ilr, st.fwi[j][h], 0x00ff00ffu);   // (a ^ b) & c
-      const std::uint32_t e1 = lop3<0x28>(ilr, st.fwi[j][h], 0xff00ff00u);
-      const std::uint32_t e1n = lop3<0x82>(ilr, st.fwi[j][h], 0xff00ff00u);  // ~(a ^ b) & c
-      PT[k][0] = mad_hi_u32(e1, st.sh24, mad_u32(x0, st.one_p, st.kc[k][0]));   // x0 + x1 + kc0
-      PT[k][1] = mad_hi_u32(e1n, st.sh24, mad_u32(x0, st.one_p, st.kc1n[k]));   // x0 - x1 + kc1
-#pragma unroll
-      for (int x = 0; x < GEO::NT; ++x) PT[k][x ^ XM] = OFFB - PT[k][x];
-    }
-  } else {
   // interleave frames A / B: lo = (A0, A1, B0, B1), hi = (A2, A3, B2, B3) of each word
   std::uint32_t il[WPB][2];
 #pragma unroll
@@ -489,9 +402,8 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
 #pragma unroll
     for (int x = 0; x < GEO::NT; ++x) {
       // T[x ^ XM] = -T[x]
-      PT[k][x ^ XM] = VD_FMA_NEG ? mad_u32(PT[k][x], st.m1, OFFB) : OFFB - PT[k][x];
+      PT[k][x ^ XM] = OFFB - PT[k][x];
     }
-  }
   }
 }
 
@@ -549,64 +461,39 @@ __device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32
 }
 
 // One block of LB stages. MODE 0 (slow) range-checks every pending store and
-// calls the stored-max argmax hook; MODE 1 / 2 are straight-line blocks whose
-// pending stores all go to shared memory / tensor memory, MODE 4 the same with
-// the target picked at run time (one code copy); MODE 3 blocks lie entirely
-// in the v1 warm-up (ACS only: no decision words, no stores).
+// calls the stored-max argmax hook; MODE 1 / 2 / 5 are straight-line blocks
+// whose pending stores all go to shared memory / tensor memory / global rows;
+// MODE 3 blocks lie entirely in the v1 warm-up (ACS only: no decision words,
+// no stores).
 template <class C, class GEO, int MODE, bool TM, bool GL, int BUF, class RecFn>
 __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
-                                          const std::uint32_t* pfA, const std::uint32_t* pfB, int pf_room,
-                                          RecFn&& rec) {
+                                          const std::uint32_t* pfA, const std::uint32_t* pfB, RecFn&& rec) {
   constexpr int LB = GEO::LB, R = GEO::R, WPB = GEO::WPB;
   constexpr std::uint32_t XM = C::kXM;
   // ---- branch-metric tables for the LB stages of this block (both frames) ---
   std::uint32_t PT[LB][1 << GEO::B];
   block_tables<C, GEO, BUF>(st, PT);
-  // Renormalisation folded into the ACS tables (VD_RENORM_TABLE): the block
+  // Renormalisation folded into the ACS tables: the block
   // after a renorm point adds st.corr = BASE - ref per half to its stage-0
   // ACS tables, which subtracts ref - BASE from every new metric (one
   // VIADD.16x2 per table entry instead of one IADD3 per state register).
   // Decision words keep the unshifted tables: both candidates shift equally.
-  constexpr bool CORR = VD_RENORM_TABLE && VD_RENORM_EVERY == 2 && BUF == 0;
+  constexpr bool CORR = BUF == 0;
   std::uint32_t PA0[1 << GEO::B];
 #pragma unroll
   for (int x = 0; x < (1 << GEO::B); ++x) PA0[x] = CORR ? __vadd2(PT[0][x], st.corr) : PT[0][x];
   auto pa = [&](int k, std::uint32_t x) { return (CORR && k == 0) ? PA0[x] : PT[k][x]; };
-  // Decision-word tables of the FMA-pipe form (see the ACS below):
-  // CN[k][x] = PT[x] - PT[x ^ XM] + 0x7FFF per half = 2 PT[x] - OFFB + 0x7FFF7FFF.
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * GEO::B) * 0x00010001u;
-  std::uint32_t CN[LB][1 << GEO::B];
-  (void)CN;
-  if constexpr (VD_DEC_FORM == 1) {
-#pragma unroll
-    for (int k = 0; k < LB; ++k) {
-#pragma unroll
-      for (int x = 0; x < (1 << GEO::B); ++x) CN[k][x] = mad_u32(PT[k][x], st.two, 0x7fff7fffu - OFFB);
-    }
-  }
   // The words of this buffer are consumed: refill it with block blk + 2 now,
   // so two full blocks of work cover the HBM latency.
-  // pf_room = words left in the frame window from pf: near the window end the
-  // prefetch is clamped so it never reads past the LLRs the caller provided.
-  if (VD_PF_SLACK || pf_room >= WPB) {
-    // VD_PF_SLACK: every launched window is followed by >= 2 blocks of
-    // readable stages (plan() / the head copies / the batch tables guarantee
-    // it), so the prefetch never needs clamping; the over-read values are
-    // never consumed past stage L-1.
+  // Every launched window is followed by >= 2 blocks of readable stages
+  // (plan() / the head copies / the batch tables guarantee it), so the
+  // prefetch never needs clamping; the over-read values are never consumed
+  // past stage L-1.
 #pragma unroll
-    for (int i = 0; i < WPB; ++i) {
-      st.llr[BUF][0][i] = ldg_pinned(pfA + i);
-      st.llr[BUF][1][i] = ldg_pinned(pfB + i);
-    }
-  } else {
-#pragma unroll
-    for (int i = 0; i < WPB; ++i) {
-      // re-read the window's last word (pf_room - 1 may be negative: still inside the
-      // frame); the values are never consumed past stage L-1.
-      const int o = i < pf_room ? i : pf_room - 1;
-      st.llr[BUF][0][i] = ldg_pinned(pfA + o);
-      st.llr[BUF][1][i] = ldg_pinned(pfB + o);
-    }
+  for (int i = 0; i < WPB; ++i) {
+    st.llr[BUF][0][i] = ldg_pinned(pfA + i);
+    st.llr[BUF][1][i] = ldg_pinned(pfB + i);
   }
   std::uint32_t tw[4];
 #pragma unroll
@@ -632,18 +519,12 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       // never reads them.)
       if constexpr (MODE == 3) {
       } else if (pair < kFmaPairs) {
-        // FMA-pipe form: (sE - sO) + (PT[x] - PT[x ^ XM] + 0x7FFF), 3 IMAD per pair
-        if constexpr (VD_DEC_FORM == 2) {
-          // d' = sE - sO + 0x7FFF - OFFB per half (one IADD3), then 2 PT + d' as
-          // IMADs with a multiplier ptxas cannot see (no CN tables)
-          const std::uint32_t dp = sE - sO + (0x7fff7fffu - OFFB);
-          w[e] = mad_u32(PT[k][x], st.two_p, dp);
-          w[od] = mad_u32(PT[k][x ^ XM], st.two_p, dp);
-        } else {
-          const std::uint32_t d = mad_u32(sO, st.m1, sE);
-          w[e] = mad_u32(d, st.one, CN[k][x]);
-          w[od] = mad_u32(d, st.one, CN[k][x ^ XM]);
-        }
+        // FMA-pipe form: (sE - sO) + (PT[x] - PT[x ^ XM] + 0x7FFF) =
+        // d' + 2 PT[x] with d' = sE - sO + 0x7FFF - OFFB per half (one IADD3),
+        // then two IMADs with a multiplier ptxas cannot see
+        const std::uint32_t dp = sE - sO + (0x7fff7fffu - OFFB);
+        w[e] = mad_u32(PT[k][x], st.two_p, dp);
+        w[od] = mad_u32(PT[k][x ^ XM], st.two_p, dp);
       } else {
         // ALU-pipe form: new - s2 (>= 0, 0 iff the second won) + 0x7FFF, 1 IADD3 each
         w[e] = nL - s2L + 0x7fff7fffu;
@@ -660,59 +541,22 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       store_dec<TM, GL>(bc, tprev, word);
       tprev = t;
       rec(t, k);
-    } else if constexpr (MODE == 1 && !VD_SMEM_DEFER) {
-      bc.drow_lane[(t - 1 - bc.s_base) * 32] = word;
-    } else if constexpr (MODE == 5 && !VD_SMEM_DEFER) {
-      bc.grow_lane[(t - 1 - bc.t_gl) * 32] = word;  // one coalesced 128-byte row per warp
     } else {
-      tw[k] = word;  // one 4-column tensor-memory store per block, below
+      tw[k] = word;  // stored after the block, below
     }
   }
   if constexpr (MODE == 2) tmem_st4(bc.taddr + static_cast<std::uint32_t>(blk * LB - 1 - bc.t_first), tw);
-  if constexpr (MODE == 6) {
-    // TMEM/smem split block (t0 == t_split): the pending stage t0 - 1 is the
-    // last TMEM column, stages t0 .. t0 + LB - 2 the first smem rows
-    tmem_st1(bc.taddr + static_cast<std::uint32_t>(blk * LB - 1 - bc.t_first), tw[0]);
-#pragma unroll
-    for (int k = 1; k < LB; ++k) bc.drow_lane[(blk * LB - 1 + k - bc.s_base) * 32] = tw[k];
-  }
-  if constexpr (MODE == 7) {
-    // first decision block (t0 <= v1 < t0 + LB): stages below v1 have no slot
-#pragma unroll
-    for (int k = 0; k < LB; ++k) {
-      const int tp = blk * LB - 1 + k;
-      if (tp >= bc.v1) {
-        if (TM) {
-          tmem_st1(bc.taddr + static_cast<std::uint32_t>(tp - bc.t_first), tw[k]);
-        } else {
-          bc.drow_lane[(tp - bc.s_base) * 32] = tw[k];
-        }
-      }
-    }
-  }
-  if constexpr (MODE == 1 && VD_SMEM_DEFER) {
+  if constexpr (MODE == 1) {
     // same register schedule as the TMEM blocks (an in-loop store per stage
     // made ptxas rotate the metric registers with ~30 IMAD.MOVs per block)
 #pragma unroll
     for (int k = 0; k < LB; ++k) bc.drow_lane[(blk * LB - 1 + k - bc.s_base) * 32] = tw[k];
   }
-  if constexpr (MODE == 5 && VD_SMEM_DEFER) {
+  if constexpr (MODE == 5) {
     // global rows: one address per block, coalesced 128-byte rows per warp
     std::uint32_t* const gp = bc.grow_lane + static_cast<std::ptrdiff_t>(blk * LB - 1 - bc.t_gl) * 32;
 #pragma unroll
     for (int k = 0; k < LB; ++k) gp[k * 32] = tw[k];
-  }
-  if constexpr (MODE == 4) {
-    // merged straight-line block: the block's 4 words go to tensor memory or
-    // to shared memory (one warp-uniform branch; one code copy for both halves
-    // of the survivor store keeps the hot loop small in the instruction cache)
-    const int tp = blk * LB - 1;
-    if (TM && tp < bc.t_split) {
-      tmem_st4(bc.taddr + static_cast<std::uint32_t>(tp - bc.t_first), tw);
-    } else {
-#pragma unroll
-      for (int k = 0; k < LB; ++k) bc.drow_lane[(tp + k - bc.s_base) * 32] = tw[k];
-    }
   }
   if constexpr (MODE != 0) tprev = blk * LB + LB - 1;
 }
@@ -766,7 +610,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
   const std::int64_t groups = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
   const std::int64_t rounds = (groups + wtotal - 1) / wtotal;
   for (std::int64_t rnd = 0; rnd < rounds; ++rnd) {
-  if (VD_LOCKSTEP && rnd > 0) __syncthreads();
+  if (rnd > 0) __syncthreads();
   const std::int64_t gwarp = rnd * wtotal + static_cast<std::int64_t>(blockIdx.x) * fp.warps_per_cta + warp;
   const std::int64_t mbase = fp.mi0 + gwarp * GEO::FPW;
   if (mbase < fp.mi1) {  // (no early return: TMEM dealloc needs every warp at the barrier)
@@ -843,27 +687,9 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     }
 #pragma unroll
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
-#pragma unroll
-    for (int j = 0; j < WPB; ++j) {
-      st.fwi[j][0] = opaque(prmt(fw[j], fw[j], 0x5410u));
-      st.fwi[j][1] = opaque(prmt(fw[j], fw[j], 0x7632u));
-    }
-#pragma unroll
-    for (int k = 0; k < LB; ++k) st.kc1n[k] = opaque(st.kc[k][1] - 0x00ff00ffu);
-    st.sh24 = fp.sh24;
-    st.one_p = fp.one;
   }
   st.two_p = fp.two;
   st.corr = 0u;
-#if VD_PARAM_MULS
-  st.one = fp.one;
-  st.two = fp.two;
-  st.m1 = fp.m1;
-#else
-  st.one = opaque(1u);
-  st.two = opaque(2u);
-  st.m1 = opaque(0xffffffffu);
-#endif
 #pragma unroll
   for (int i = 0; i < R; ++i) st.sig[i] = BASE;
 #pragma unroll
@@ -881,10 +707,6 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
   // Prefetch pointers: block b + 2 is requested right after block b has
   // built its tables (two blocks of latency cover).
   const std::uint32_t* pfA = llrA + 2 * WPB;
-  // words of the frame window [0, L) stages: the word holding stage L-1 is the
-  // last one read (plan() keeps 2 stages of slack after every fast frame).
-  const int pf_last = (L * B - 1) / 4 + 1;  // one past the last word
-  int pf_off = 2 * WPB;
   const std::uint32_t* pfB = llrB + 2 * WPB;
 
   int next_sub = 0;
@@ -962,20 +784,14 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
   const std::uint32_t* const xr = xbuf + opaque(static_cast<std::uint32_t>(grp * GEO::XSTRIDE + lam * GEO::LSTRIDE));
   auto block_end = [&](int blk, auto buf_tag) {
     // ---- renormalisation every 2 blocks (after each odd block: a compile-time
-    // position in the 2-block loop body) or every 4 blocks (group-wide
-    // reference): metrics stay within [BASE - spread, BASE + spread + 16 * 510]
-    // (< 32768 up to K = 9).
+    // position in the 2-block loop body; group-wide reference): metrics stay
+    // within [BASE - spread, BASE + spread + 16 * 510] (< 32768 up to K = 9).
     constexpr int BUFE = decltype(buf_tag)::value;
-    if (VD_RENORM_EVERY == 2 ? BUFE == 1 : (blk & 3) == 3) {
+    if (BUFE == 1) {
       const std::uint32_t ref = __shfl_sync(kFull, st.sig[0], grp * G);
       subA += static_cast<std::int32_t>(ref & 0xffffu) - 8192;
       subB += static_cast<std::int32_t>(ref >> 16) - 8192;
-      if constexpr (VD_RENORM_TABLE && VD_RENORM_EVERY == 2) {
-        st.corr = __vsub2(BASE, ref);  // applied by the next (BUF 0) block's stage-0 tables
-      } else {
-#pragma unroll
-        for (int i = 0; i < R; ++i) st.sig[i] = st.sig[i] - ref + BASE;
-      }
+      st.corr = __vsub2(BASE, ref);  // applied by the next (BUF 0) block's stage-0 tables
     }
     // ---- relayout: back to the canonical layout (P_new = rotr(P_old, r)) --
     if constexpr (GEO::kChunked) {
@@ -1024,56 +840,23 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       __syncwarp();
     }
   };
-  auto one_block = [&](int blk, auto buf_tag) {
-    constexpr int BUF = decltype(buf_tag)::value;
-    const int t0 = blk * LB;
-    // Straight-line block: pending stores (stages t0-1 .. t0+LB-2) all inside
-    // [v1, L) and on one side of the TMEM/smem split, no start stage inside.
-    const bool clean = (t0 - 1 >= v1) && (t0 + LB - 2 < L) && !(next_rec >= t0 && next_rec < t0 + LB);
-    if (t0 + LB <= v1) {
-      // warm-up block: every stage (and the next block's pending one) < v1
-      run_block<C, GEO, 3, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    } else if (VD_MERGED_STORE && clean && (!GL || t0 + LB - 2 < t_gl) && (t0 - 1 >= t_split || (TM && t0 + LB - 2 < t_split))) {
-      run_block<C, GEO, 4, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    } else if (GL && clean && t0 - 1 >= t_gl) {
-      run_block<C, GEO, 5, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    } else if (clean && t0 - 1 >= t_split && (!GL || t0 + LB - 2 < t_gl)) {
-      run_block<C, GEO, 1, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    } else if (TM && clean && t0 + LB - 2 < t_split) {
-      run_block<C, GEO, 2, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    } else {
-      run_block<C, GEO, 0, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    }
-    pf_off += WPB;
-    pfA += WPB;
-    pfB += WPB;
-    block_end(blk, buf_tag);
-  };
-#if VD_RUNS && !VD_MERGED_STORE
-  // The store mode of a block (one_block's tests) only changes at a few block
-  // indices per frame: the end of the warm-up, the first / last clean block,
+  // Store mode of a block: warm-up (3: t0 + LB <= v1); straight-line
+  // ("clean": pending stores of stages t0-1 .. t0+LB-2 all inside [v1, L) and
+  // on one side of the TMEM / smem / global split, no start stage inside) to
+  // global rows (5), smem rows (1) or TMEM (2); else the general block (0).
+  // The mode only changes at a few block indices per frame: the end of the warm-up, the first / last clean block,
   // the TMEM / smem / global-row splits, and the block holding the next
   // stored-max start stage (which only moves inside a MODE 0 block). The loop
   // picks the mode once per run of equal-mode blocks and runs them with a
-  // fixed body (same blocks, same modes, same order as one_block).
+  // fixed body (per-block mode tests had cost ~40 instructions per block pair).
   auto one_block_mode = [&](int blk, auto mode_tag, auto buf_tag) {
     constexpr int MD = decltype(mode_tag)::value, BUF = decltype(buf_tag)::value;
-    run_block<C, GEO, MD, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, pf_last - pf_off, rec);
-    pf_off += WPB;
+    run_block<C, GEO, MD, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
     pfA += WPB;
     pfB += WPB;
     block_end(blk, buf_tag);
   };
   auto run_mode = [&](auto mode_tag, int& blk, int end) {
-#if VD_RUN_LOOP1
-    for (; blk < end; ++blk) {  // one block per iteration, body by parity (no loop break)
-      if ((blk & 1) == 0) {
-        one_block_mode(blk, mode_tag, std::integral_constant<int, 0>{});
-      } else {
-        one_block_mode(blk, mode_tag, std::integral_constant<int, 1>{});
-      }
-    }
-#else
     while (blk < end) {
       if ((blk & 1) == 0) {
         one_block_mode(blk, mode_tag, std::integral_constant<int, 0>{});
@@ -1082,7 +865,6 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       one_block_mode(blk, mode_tag, std::integral_constant<int, 1>{});
       ++blk;
     }
-#endif
   };
   // first block index with blk * LB + LB - 2 >= x  /  with blk * LB - 1 >= x
   auto first_hi = [](int x) { return (x + 1) / LB; };
@@ -1101,12 +883,6 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     if (blk < nb_warm) {
       md = 3;
       end = nb_warm;
-    } else if (VD_EDGE_MODES && blk < cl_lo && blk < cl_hi && blk != rb &&
-               (TM ? blk * LB + LB - 2 < t_split : (!GL || blk * LB + LB - 2 < t_gl))) {
-      md = 7;  // the one block with t0 <= v1 < t0 + LB
-    } else if (VD_EDGE_MODES && TM && blk * LB == t_split && blk >= cl_lo && blk < cl_hi && blk != rb &&
-               (!GL || blk * LB + LB - 2 < t_gl)) {
-      md = 6;
     } else if (blk >= cl_lo && blk < cl_hi && blk != rb) {
       const int rend = rb > blk ? min(cl_hi, rb) : cl_hi;
       if (GL && blk >= gl_lo) {
@@ -1128,21 +904,10 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       run_mode(std::integral_constant<int, 3>{}, blk, end);
     } else if (GL && md == 5) {
       run_mode(std::integral_constant<int, 5>{}, blk, end);
-    } else if (VD_EDGE_MODES && md == 7) {
-      run_mode(std::integral_constant<int, 7>{}, blk, end);
-    } else if (VD_EDGE_MODES && TM && md == 6) {
-      run_mode(std::integral_constant<int, 6>{}, blk, end);
     } else {
       run_mode(std::integral_constant<int, 0>{}, blk, end);
     }
   }
-  (void)one_block;
-#else
-  for (int blk = 0; blk < nblk; blk += 2) {
-    one_block(blk, std::integral_constant<int, 0>{});
-    if (blk + 1 < nblk) one_block(blk + 1, std::integral_constant<int, 1>{});
-  }
-#endif
   // decisions of the last processed stage
   store_dec<TM, GL>(bc, tprev, compact16(st.wv[(nblk * LB - 1) & 1]));
   if constexpr (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -1195,25 +960,20 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       std::uint32_t* const outw = p.out + ((obase + v1) >> 5);
       const int t_emit = v1 + f;  // blocks below this stage emit their 4 bits
       std::uint32_t* wp = outw + ((t_emit - LB - v1) >> 5);  // word of the first emitting block
-      (void)wp;
       auto step_block = [&](int tb0, const std::uint32_t (&wd)[LB], int jmax = 3 /* LB - 1 */) {
         const std::uint32_t rin = u & (R - 1);  // bit j = decoded bit of stage tb0 + j
 #pragma unroll
         for (int j = LB - 1; j >= 0; --j) {
           const std::uint32_t x = __funnelshift_r(wd[j], wd[j], u - static_cast<std::uint32_t>(j));  // bit u -> bit j
-          if (j <= jmax) u = VD_TB_BITSEL ? bitsel_m(x, u, 1u << j) : (x & (1u << j)) | (u & ~(1u << j));
+          if (j <= jmax) u = bitsel_m(x, u, 1u << j);
         }
         if (tb0 < t_emit) {
           acc32 = (acc32 << LB) | rin;
-#if VD_TB_WP
           // running word pointer (one decrement per store, no address math per block)
           if (((tb0 - v1) & 31) == 0) {
             if (valid) *wp = acc32;
             --wp;
           }
-#else
-          if (((tb0 - v1) & 31) == 0 && valid) outw[(tb0 - v1) >> 5] = acc32;
-#endif
         }
         const std::uint32_t pa = (lp << r) | (u & (R - 1));
         const std::uint32_t pn = ((pa << r) | (pa >> (M - r))) & GEO::SMASK;  // undo the block relayout
@@ -1292,38 +1052,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
           }
         }
       }
-      bool smem_done = false;
-#if VD_TB_SMEM_PIPE
-      if constexpr (G == 4) {
-        // shared-memory rows, one block ahead: the group's 4 words of a stage
-        // are one 16-byte load that does not depend on the traced lane
-        smem_done = true;
-        if (tb0 >= v1 && (!TM || tb0 >= t_split)) {
-          const std::uint32_t* grp_row = dec + gcol - s_base * 32;
-          uint4 cur[LB];
-#pragma unroll
-          for (int j = 0; j < LB; ++j) cur[j] = *reinterpret_cast<const uint4*>(grp_row + (tb0 + j) * 32);
-          for (; tb0 >= v1 && (!TM || tb0 >= t_split); tb0 -= LB) {
-            uint4 nxt[LB];
-            const bool more = tb0 - LB >= v1 && (!TM || tb0 - LB >= t_split);
-#pragma unroll
-            for (int j = 0; j < LB; ++j)
-              nxt[j] = more ? *reinterpret_cast<const uint4*>(grp_row + (tb0 - LB + j) * 32) : cur[j];
-            std::uint32_t wd[LB];
-#pragma unroll
-            for (int j = 0; j < LB; ++j) {
-              const uint4 c = cur[j];
-              const std::uint32_t lo = (lp & 1u) ? c.y : c.x, hi = (lp & 1u) ? c.w : c.z;
-              wd[j] = (lp & 2u) ? hi : lo;
-            }
-            step_block(tb0, wd);
-#pragma unroll
-            for (int j = 0; j < LB; ++j) cur[j] = nxt[j];
-          }
-        }
-      }
-#endif
-      if (!smem_done) {
+      {
         for (; tb0 >= v1 && (!TM || tb0 >= t_split); tb0 -= LB) {  // shared-memory rows
           std::uint32_t wd[LB];
           const std::uint32_t* src = dec + (tb0 - s_base) * 32 + gcol + lp;
@@ -1333,26 +1062,6 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         }
       }
       if constexpr (TM) {
-#if VD_TB_TMEM_PIPE
-        // tensor-memory columns, one block ahead: the 4-column load of the
-        // next block does not depend on the traced state, so it is issued
-        // before this block's shuffles / steps and waited for after them
-        if (tb0 >= v1) {
-          std::uint32_t own[4];
-          tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
-          for (; tb0 >= v1; tb0 -= LB) {
-            std::uint32_t nxt[4] = {0u, 0u, 0u, 0u}, wd[LB];
-            const bool more = tb0 - LB >= v1;
-            if (more) tmem_ld4_async(bc.taddr + static_cast<std::uint32_t>(tb0 - LB - t_first), nxt);
-#pragma unroll
-            for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
-            step_block(tb0, wd);
-            if (more) tmem_wait_ld(nxt);
-#pragma unroll
-            for (int j = 0; j < 4; ++j) own[j] = nxt[j];
-          }
-        }
-#else
         for (; tb0 >= v1; tb0 -= LB) {  // tensor-memory columns
           std::uint32_t own[4], wd[LB];
           tmem_ld4(bc.taddr + static_cast<std::uint32_t>(tb0 - t_first), own);
@@ -1360,7 +1069,6 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
           for (int j = 0; j < LB; ++j) wd[j] = __shfl_sync(kFull, own[j], gcol + static_cast<int>(lp));
           step_block(tb0, wd);
         }
-#endif
       }
       continue;
     }
@@ -1377,7 +1085,6 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       std::uint32_t acc32 = 0;
       std::uint32_t* const outw = p.out + ((obase + sub_lo) >> 5);
       std::uint32_t* wp = outw + ((sub_hi - LB - sub_lo) >> 5);  // word of this lane's first emitting block
-      (void)wp;
       const int tstart = static_cast<int>(__reduce_max_sync(kFull, active ? static_cast<unsigned>(stb) : 0u));
       const int tstop = static_cast<int>(__reduce_min_sync(kFull, active ? static_cast<unsigned>(sub_lo) : 0x7fffffffu));
       for (int tb0 = tstart; tb0 >= tstop; tb0 -= LB) {
@@ -1401,18 +1108,14 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         for (int j = LB - 1; j >= 0; --j) {
           const std::uint32_t x = __funnelshift_r(wd[j], wd[j], u - static_cast<std::uint32_t>(j));
           const bool walk = act && (j <= ph || !top);
-          if (walk) u = VD_TB_BITSEL ? bitsel_m(x, u, 1u << j) : (x & (1u << j)) | (u & ~(1u << j));
+          if (walk) u = bitsel_m(x, u, 1u << j);
         }
         if (act && tb0 < sub_hi) {
           acc32 = (acc32 << LB) | rin;
-#if VD_TB_WP
           if (((tb0 - sub_lo) & 31) == 0) {
             if (valid) *wp = acc32;
             --wp;
           }
-#else
-          if (((tb0 - sub_lo) & 31) == 0 && valid) outw[(tb0 - sub_lo) >> 5] = acc32;
-#endif
         }
         if (act) {
           const std::uint32_t pa = (lp << r) | (u & (R - 1));
@@ -1594,10 +1297,7 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   fp.llr_head = p.llr_head;
   fp.head_pitch = p.head_pitch;
   fp.p = p;
-  fp.one = 1u;
   fp.two = 2u;
-  fp.m1 = 0xffffffffu;
-  fp.sh24 = 1u << 24;
   fp.L = p.f + p.v1 + p.v2;
   fp.nblk = (fp.L + GEO::LB - 1) / GEO::LB;
   fp.step = p.f0 > 0 ? p.f0 : p.f;
@@ -1617,9 +1317,8 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
     if (p.sigma) return false;
   } else {
   // stages read per frame: the window rounded up to whole blocks, plus the
-  // two-block prefetch overrun when VD_PF_SLACK (else 4 stages of word slack)
-  const std::int64_t span = VD_PF_SLACK ? static_cast<std::int64_t>(fp.nblk) * GEO::LB + 2 * GEO::LB
-                                        : static_cast<std::int64_t>(fp.L) + 4;
+  // two-block prefetch overrun
+  const std::int64_t span = static_cast<std::int64_t>(fp.nblk) * GEO::LB + 2 * GEO::LB;
   std::int64_t lo = pad_head ? p.frame_begin : (p.v1 + p.f - 1) / p.f;  // first m with m*f >= v1 (or padded head)
   std::int64_t hi_excl = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // m*f + f + v2 <= n
   // the caller guarantees LLRs up to the window end of the last launched frame
