@@ -5,18 +5,28 @@
 
 Workload (BASELINE.json configs[4], "C5"): K=7 (171,133) rate 1/2, int8 LLRs
 (scale 32, Eb/N0 3 dB, synthetic, generated in HBM), frames f=256, v1=v2=20,
-serial traceback. A step decodes the rank's whole resident stream of
---stages stages (default 2^32 = 4 Gi info bits per GPU; weak scaling: each
-rank owns its own stream, frames are independent, no collective on the data
-path). Inputs (8 GiB) exceed L2, so no flush is needed between steps.
+serial traceback. A step decodes ONE stream of --stages stages (default
+2^32 = 4 Gi info bits) sharded over the N ranks (strong scaling, BASELINE C5
+"4G info bits sharded across 1/2/4/8"): rank r owns a contiguous, output-word
+aligned frame range (vd_partition_frames) and holds only its LLR window (the
+frames' stages plus the v1 / v2 halo, synthesised on its own device: every
+value is a pure function of (seed, stage)); no collective on the data path.
+After timing, rank 0 gathers the packed slices and checks them against its
+own 1-GPU decode of the whole stream (identity_vs_1gpu_decode). A secondary
+weak-scaling line (every rank its own whole stream) is added for N > 1.
+Inputs (8 GiB at N = 1) exceed L2, so no flush is needed between steps.
 
 value: device-timed (CUDA events on the decode stream, max over ranks)
-       whole-job info bits / s.
+       whole-stream info bits / s.
 e2e:   the same metric through the reference-facing host call
        (vd_decode_i8: pinned host LLRs -> H2D -> kernel -> D2H packed bits,
-       streamed in chunks), timed per step around the call.
-roofline: the decode kernel against its binding roof (integer ALU; the HBM
-       roof is reported alongside), see DESIGN.md §4.
+       streamed in chunks; each rank its 1/N share), timed around the call.
+roofline: the decode kernel against its binding roof (integer ALU: the
+       measured ACS-pair rate of profiles/alu_peak.json, and the dual-issue
+       bound; the HBM roof alongside), see DESIGN.md §4. traffic: DRAM bytes
+       of this round's ncu capture (profiles/decode_traffic.json).
+gpu_launches: kernels this library launched inside the timed region
+       (vd_kernel_launches() counter around it).
 cpu_baseline: the reference's own framed_decode (oracle/_ref, compiled from
        the reference sources) with all host threads, on a bounded sample.
 """
@@ -64,6 +74,7 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--cpu-seconds", type=float, default=8.0, help="target wall time of the CPU baseline sample")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-weak", action="store_true", help="skip the secondary weak-scaling line (N > 1)")
     ap.add_argument("--frame", default="", help="f,v1,v2[,f0] frame configuration override (default 256,20,20)")
     a = ap.parse_args()
     if a.frame:
@@ -143,59 +154,76 @@ class ClockSampler:
 
 # ------------------------------------------------------------ CPU arms -----
 
-def cpu_reference_rate(target_s: float, threads: int | None = None, code=K7):
-    """The reference framed_decode (oracle/_ref, all host threads) or, if the
-    reference library is absent, the single-threaded C oracle port. Returns
-    (Gbps, cores, kind, sample description)."""
-    import numpy as np
+class CpuArm:
+    """The reference's own framed_decode (oracle/_ref, compiled from the
+    reference sources, all host threads) or, if that library is absent, the
+    single-threaded C oracle port, on a bounded sample of the workload: a
+    contiguous stream of `n` info bits from the reference's data chain
+    (random_bits -> encode -> BPSK -> AWGN, berlab.cpp:138-142), int8-quantised
+    (q = rint(32 y)) and handed to framed_decode as doubles."""
 
-    import oracle
+    def __init__(self, code, n=None, target_s=8.0, threads=None):
+        import oracle
 
-    port = oracle.port()
-    ref = oracle.ref_backend()
-    cores = threads or os.cpu_count() or 1
-    kind = "reference" if ref is not None else "port"
-    if ref is None:
-        cores = 1
-    backend = ref if ref is not None else port
-    # probe on a small block, then size the sample for ~target_s of wall time
-    n = 1 << 16
-    rx, _ = port.gen_bench_block(*code, n, EBN0, 1)
-    q = oracle.quantize(rx, SCALE)
-    t0 = time.perf_counter()
-    backend.framed_decode(*code, q, n, F, V1, V2, F0, workers=cores)
-    rate = n / max(time.perf_counter() - t0, 1e-6)
-    n = int(min(max(rate * target_s, 1 << 16), 1 << 26))
-    rx, _ = port.gen_bench_block(*code, n, EBN0, 2)
-    q = oracle.quantize(rx, SCALE)
-    t0 = time.perf_counter()
-    backend.framed_decode(*code, q, n, F, V1, V2, F0, workers=cores)
-    dt = time.perf_counter() - t0
-    sample = (f"{n} info bits (K={code[0]} B={code[1]}, int8 q=rint(32y) at {EBN0} dB, f={F}/v1={V1}/v2={V2}/f0={F0}), "
-              f"{'reference framed_decode, workers=' + str(cores) if ref else 'C oracle port, 1 thread'}")
-    return n / dt / 1e9, cores, kind, sample, dt
+        self.code = code
+        self.port = oracle.port()
+        ref = oracle.ref_backend()
+        self.kind = "reference" if ref is not None else "port"
+        self.backend = ref if ref is not None else self.port
+        self.cores = (threads or os.cpu_count() or 1) if ref is not None else 1
+        if n is None:
+            # probe the rate, then size the sample for ~target_s (>= 2^26 bits
+            # when that fits in 4 x target_s, SURVEY §8(d): ">= 64 Mi-bit prefix")
+            m = 1 << 16
+            q = self._gen(m, 1)
+            t0 = time.perf_counter()
+            self._decode(q, m)
+            rate = m / max(time.perf_counter() - t0, 1e-6)
+            n = int(min(max(rate * target_s, 1 << 16), 1 << 28))
+            if n < (1 << 26) and rate * 4 * target_s >= (1 << 26):
+                n = 1 << 26
+        self.n = n
+        self.q = self._gen(n, 2)
+
+    def _gen(self, n, seed):
+        import oracle
+
+        rx, _ = self.port.gen_bench_block(*self.code, n, EBN0, seed)
+        return oracle.quantize(rx, SCALE)
+
+    def _decode(self, q, n):
+        self.backend.framed_decode(*self.code, q, n, F, V1, V2, F0, workers=self.cores)
+
+    def time_once(self):
+        t0 = time.perf_counter()
+        self._decode(self.q, self.n)
+        return time.perf_counter() - t0
+
+    def sample(self):
+        k, b = self.code[0], self.code[1]
+        who = f"reference framed_decode, workers={self.cores}" if self.kind == "reference" else "C oracle port, 1 thread"
+        return (f"{self.n} info bits (K={k} B={b}, int8 q=rint(32y) at {EBN0} dB, f={F}/v1={V1}/v2={V2}/f0={F0}), "
+                f"{who}")
 
 
 def run_reference_arm(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    per_step = []
-    info = None
-    for i in range(args.warmup + args.steps):
-        info = cpu_reference_rate(min(args.cpu_seconds, 20.0) / 4)
-        if i >= args.warmup:
-            per_step.append(info)
-    gbps = sorted(x[0] for x in per_step)[len(per_step) // 2]
-    _, cores, kind, sample, dt = per_step[-1]
+    arm = CpuArm(args.code, target_s=min(args.cpu_seconds, 20.0) / 4)
+    for _ in range(args.warmup):
+        arm.time_once()
+    dts = sorted(arm.time_once() for _ in range(args.steps))
+    dt = dts[len(dts) // 2]  # median step
+    gbps = arm.n / dt / 1e9
     line = {
         "metric": "decoded info Gbps (K=7 r1/2 soft)", "value": gbps, "unit": "Gbps", "impl": "reference",
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic (reference random_bits/encode/BPSK/AWGN chain, int8-quantised)",
-        "config": {"workload": "K=7 r1/2 (171,133) framed f=256 v1=20 v2=20, CPU sample per step",
-                   "sample": sample},
-        "cpu_baseline": {"value": gbps, "unit": "Gbps", "cores": cores, "kind": kind, "sample": sample},
+        "config": {"workload": "K=7 r1/2 (171,133) framed f=256 v1=20 v2=20, CPU sample per step (median step)",
+                   "sample": arm.sample()},
+        "cpu_baseline": {"value": gbps, "unit": "Gbps", "cores": arm.cores, "kind": arm.kind, "sample": arm.sample()},
         "e2e": {"value": gbps, "unit": "Gbps", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line))
@@ -209,20 +237,52 @@ def alu_ops_per_bit(stats_stages: int, n: int, s: int = 64) -> float:
     return 3.0 * s * stats_stages / n
 
 
+def alu_peaks(sms: int, sm_mhz: float):
+    """(measured ACS-pair Tops, its source, dual-issue bound Tops). The
+    measured rate is profiles/alu_peak.json (microbench/run_alu_peak.py on a
+    B200: the fast kernel's VIADD.16x2 -> VIADDMNMX.S16x2 pair); the dual-issue
+    bound is 1 warp-instruction / clk / SMSP with the fmaheavy and alu pipes
+    each at 0.5 (profiles/r01_pipe_probe_ncu.csv) x 3 lane-ops per packed
+    instruction = 384 lane-ops / clk / SM."""
+    dual = sms * 384 * sm_mhz * 1e6 / 1e12
+    p = ROOT / "profiles" / "alu_peak.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        if "acs_warp_instr_per_sm_clk" in d:
+            tops = d["lane_ops_per_sm_clk"] * sms * sm_mhz * 1e6 / 1e12
+            src = (f"profiles/alu_peak.json: ACS pair measured at {d['acs_warp_instr_per_sm_clk']:.3f} warp-instr/SM/clk "
+                   f"({d['lane_ops_per_sm_clk']:.0f} lane-ops/clk/SM) x {sms} SM x {sm_mhz:.0f} MHz")
+            return tops, src, dual
+    return dual, "dual-issue bound (profiles/alu_peak.json absent)", dual
+
+
+def kernel_traffic(workload: str):
+    """DRAM bytes per decoded bit of the decode kernel from this round's ncu
+    capture (tools/ncu_traffic.py -> profiles/decode_traffic.json), or None."""
+    tp = ROOT / "profiles" / "decode_traffic.json"
+    if not tp.exists():
+        return None, None
+    d = json.loads(tp.read_text())
+    w = d.get("workloads", {}).get(workload)
+    if not w:
+        return None, None
+    return w["bytes_per_bit"], d.get("source")
+
+
 def run_ours(args):
     import numpy as np
     import torch
 
     import paper_2011_09337_b200 as vd
-    from paper_2011_09337_b200.device import decode_i8_device, synth_llr_i8
+    from paper_2011_09337_b200.device import count_bit_errors, decode_i8_device, synth_llr_i8_range
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     # Plumbing test hook: VITDEC_BENCH_ONE_DEVICE=1 puts every rank on cuda:0
     # with the gloo backend (NCCL refuses two ranks on one GPU), so the N > 1
-    # path (barriers, max-over-ranks timing, rank-0 reporting) can be exercised
-    # on a one-GPU box. Numbers from such a run are not scaling measurements.
+    # path (shards, barriers, max-over-ranks timing, identity gather, rank-0
+    # reporting) can be exercised on a one-GPU box. Not a scaling measurement.
     one_dev = os.environ.get("VITDEC_BENCH_ONE_DEVICE") == "1"
     if one_dev:
         local = 0
@@ -238,37 +298,58 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     red_dev = torch.device("cpu") if one_dev else dev  # gloo reduces CPU tensors
 
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        tt = torch.tensor([x], dtype=torch.float64, device=red_dev)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        return float(tt.item())
+
     t = vd.build_trellis(vd.CodeSpec(*args.code))
     B = args.code[1]
+    S = 1 << (args.code[0] - 1)
     cfg = vd.FrameConfig(F, V1, V2, F0)
-    n = args.stages
+    n = args.stages  # the WHOLE stream (strong scaling: shared by the ranks)
     nf = (n + F - 1) // F
-    stats = vd.frame_stats(cfg, n)
+    sigma = (1.0 / (2 * (1.0 / B) * 10 ** (EBN0 / 10))) ** 0.5
+    seed = 1234
     stream = torch.cuda.Stream(device=dev)
-    llr = torch.empty(n * B, dtype=torch.int8, device=dev)
-    bits = torch.empty((n + 31) // 32, dtype=torch.int32, device=dev)
-    out = torch.empty((n + 31) // 32 + 1, dtype=torch.int32, device=dev)
+
+    # ---- this rank's shard: contiguous word-aligned frames + v1/v2 halo -----
+    first = vd.partition_frames(cfg, n, world)
+    fb, fe = first[rank], first[rank + 1]
+    wb, we = vd.frame_window(cfg, n, fb, fe) if fe > fb else (0, 0)
+    out0, out1 = fb * F, min(fe * F, n)
+    llr = torch.empty(max(we - wb, 1) * B, dtype=torch.int8, device=dev)
+    words = (out1 - out0 + 31) // 32
+    out = torch.empty(words + 1, dtype=torch.int32, device=dev)
+    bits = torch.empty(words + 1, dtype=torch.int32, device=dev)
     with torch.cuda.stream(stream):
-        synth_llr_i8(t, n, (1.0 / (2 * (1.0 / B) * 10 ** (EBN0 / 10))) ** 0.5, SCALE, 1234 + rank, llr, bits, local, stream)
+        if fe > fb:
+            synth_llr_i8_range(t, wb, we - wb, sigma, SCALE, seed, llr, None, local, stream)
+            synth_llr_i8_range(t, out0, out1 - out0, sigma, SCALE, seed, None, bits, local, stream)
     stream.synchronize()
 
     def step():
-        decode_i8_device(t, cfg, n, llr, 0, 0, nf, out, 0, None, local, stream)
+        if fe > fb:
+            decode_i8_device(t, cfg, n, llr, wb, fb, fe, out, out0, None, local, stream)
 
     for _ in range(args.warmup):
         step()
     stream.synchronize()
-    # correctness guard on the timed data: decoded vs sent BER must be sane
     cnt = torch.zeros(1, dtype=torch.int64, device=dev)
-    vd.device.count_bit_errors(out, bits, n, cnt, local, stream)
+    if fe > fb:
+        count_bit_errors(out, bits, out1 - out0, cnt, local, stream)
     stream.synchronize()
-    ber = int(cnt.item()) / n
+    errs = int(cnt.item())
 
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
+    lib = vd.lib()
+    l0 = lib.vd_kernel_launches()
     with ClockSampler(local) as clk:
         ev0.record(stream)
         for _ in range(args.steps):
@@ -276,22 +357,92 @@ def run_ours(args):
         ev1.record(stream)
         ev1.synchronize()
     torch.cuda.synchronize()
-    ms = ev0.elapsed_time(ev1)
+    launches = (lib.vd_kernel_launches() - l0) / args.steps  # this rank's kernels per step
+    ms = max_over_ranks(ev0.elapsed_time(ev1))
     if dist:
-        tt = torch.tensor([ms], device=red_dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms = float(tt.item())
         dist.barrier()
     ms_step = ms / args.steps
-    total_bits = n * world
-    gbps = total_bits / (ms_step * 1e-3) / 1e9
+    gbps = n / (ms_step * 1e-3) / 1e9  # whole stream / slowest rank
+
+    # ---- 1-GPU identity (N > 1): rank 0 decodes the whole stream alone ----
+    identity = None
+    if dist:
+        tot = torch.tensor([errs], dtype=torch.int64, device=red_dev)
+        dist.all_reduce(tot)
+        errs = int(tot.item())
+        maxw = (max(min(first[r + 1] * F, n) - first[r] * F for r in range(world)) + 31) // 32
+        mine = torch.zeros(maxw, dtype=torch.int32, device=red_dev)
+        mine[:words] = out[:words].to(red_dev)
+        gathered = [torch.empty_like(mine) for _ in range(world)] if rank == 0 else None
+        if one_dev:
+            dist.gather(mine, gathered, dst=0)
+        else:
+            allg = [torch.empty_like(mine) for _ in range(world)]
+            dist.all_gather(allg, mine)
+            gathered = allg if rank == 0 else None
+        if rank == 0:
+            del llr
+            torch.cuda.empty_cache()
+            full_llr = torch.empty(n * B, dtype=torch.int8, device=dev)
+            full_out = torch.empty((n + 31) // 32 + 1, dtype=torch.int32, device=dev)
+            synth_llr_i8_range(t, 0, n, sigma, SCALE, seed, full_llr, None, local, stream)
+            decode_i8_device(t, cfg, n, full_llr, 0, 0, nf, full_out, 0, None, local, stream)
+            stream.synchronize()
+            ok = True
+            for r in range(world):
+                a0, a1 = first[r] * F, min(first[r + 1] * F, n)
+                w = (a1 - a0 + 31) // 32
+                if w == 0:
+                    continue
+                ref = full_out[a0 // 32:a0 // 32 + w].cpu()
+                ok &= bool(torch.equal(gathered[r][:w].cpu(), ref))
+            identity = ok
+            del full_llr, full_out
+            torch.cuda.empty_cache()
+        dist.barrier()
+
+    # ---- weak scaling (secondary, N > 1): every rank its own whole stream ---
+    weak = None
+    if dist and not args.no_weak:
+        nw = n
+        del out, bits
+        if rank != 0:
+            del llr
+        torch.cuda.empty_cache()
+        wl = torch.empty(nw * B, dtype=torch.int8, device=dev)
+        wo = torch.empty((nw + 31) // 32 + 1, dtype=torch.int32, device=dev)
+        synth_llr_i8_range(t, 0, nw, sigma, SCALE, seed + 1 + rank, wl, None, local, stream)
+        wstep = lambda: decode_i8_device(t, cfg, nw, wl, 0, 0, (nw + F - 1) // F, wo, 0, None, local, stream)
+        for _ in range(args.warmup):
+            wstep()
+        stream.synchronize()
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            wstep()
+        e1.record(stream)
+        e1.synchronize()
+        wms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
+        weak = {"value": nw * world / (wms * 1e-3) / 1e9, "unit": "Gbps", "ms_per_step": wms,
+                "info_bits_per_gpu_per_step": nw, "scaling": "weak"}
+        del wl, wo
+        torch.cuda.empty_cache()
+        dist.barrier()
 
     # ---- e2e through the host-buffer C-ABI call (pinned memory) -----------
-    ne = min(args.e2e_stages, n)
+    # every rank streams its 1/N share of the e2e stream (an independent
+    # sub-stream, own frame grid) from pinned host memory: H2D -> decode ->
+    # D2H of the packed bits, inside the timed region
+    ne_total = min(args.e2e_stages, n)
+    ne = max(((ne_total // world) // 32) * 32, 32)
+    e2e_llr = torch.empty(ne * B, dtype=torch.int8, device=dev)
+    synth_llr_i8_range(t, rank * ne, ne, sigma, SCALE, seed, e2e_llr, None, local, stream)
+    stream.synchronize()
     host_llr = torch.empty(ne * B, dtype=torch.int8, pin_memory=True)
-    host_llr.copy_(llr[: ne * B])
+    host_llr.copy_(e2e_llr)
     host_out = torch.empty((ne + 31) // 32, dtype=torch.int32, pin_memory=True)
-    lib = vd.lib()
     c = cfg.to_c()
     dev_idx = C.c_int32(local)
     ex = vd._lib.VdExec(1, C.pointer(dev_idx), 0)
@@ -302,51 +453,44 @@ def run_ours(args):
                                        C.byref(st), C.byref(ex)))
 
     e2e_step()
+    # the e2e result must equal the device-resident decode of the same stream
+    chk = torch.empty((ne + 31) // 32 + 1, dtype=torch.int32, device=dev)
+    decode_i8_device(t, cfg, ne, e2e_llr, 0, 0, (ne + F - 1) // F, chk, 0, None, local, stream)
+    stream.synchronize()
+    same = bool(torch.equal(host_out, chk[:(ne + 31) // 32].cpu()))
+    del e2e_llr, chk
     if dist:
         dist.barrier()
     e2e_reps = max(args.e2e_steps, 1)
     t0 = time.perf_counter()
     for _ in range(e2e_reps):
         e2e_step()
-    e2e_s = (time.perf_counter() - t0) / e2e_reps
-    if dist:
-        tt = torch.tensor([e2e_s], device=red_dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        e2e_s = float(tt.item())
+    e2e_s = max_over_ranks((time.perf_counter() - t0) / e2e_reps)
     e2e_gbps = ne * world / e2e_s / 1e9
-    # e2e result must equal the device-resident decode of the same prefix
-    words = ne // 32
-    same = bool(torch.equal(host_out[:words], out[:words].cpu()))
 
     # ---- roofline ----------------------------------------------------------
-    # Binding roof: integer ALU. The packed ACS (VIADD.16x2 on the fmaheavy
-    # pipe + VIADDMNMX.S16x2 on the alu pipe, each 0.5 warp-instr/clk/SMSP as
-    # measured with ncu in profiles/r01_pipe_probe_ncu.csv) retires 2 states x
-    # 3 ops per instruction pair: 4 SMSP x 32 lanes x 0.5 x 6 = 384 lane-ops
-    # per SM clock. HBM roof reported alongside.
     peaks, peak_src = measured_peaks()
     clocks = clk.summary()
     sm_mhz = clocks.get("sm_mhz") or peaks.get("sm_max_mhz", 1965.0)
     sms = torch.cuda.get_device_properties(dev).multi_processor_count
-    alu_peak = sms * 384 * sm_mhz * 1e6 / 1e12
-    alu_src = (f"{sms} SM x 384 packed-ACS lane-ops/clk (ncu-measured pipe rates, profiles/r01_pipe_probe_ncu.csv) "
-               f"x {sm_mhz:.0f} MHz (median SM clock during the timed region)")
-    ops_bit = alu_ops_per_bit(stats.stages, n, 1 << (args.code[0] - 1))
-    bits_per_s_kernel = n / (ms_step * 1e-3)
-    alu_achieved = ops_bit * bits_per_s_kernel / 1e12
-    hbm_bytes = n * B + n / 8  # int8 LLR read once + packed output
-    hbm_achieved = hbm_bytes / (ms_step * 1e-3) / 1e9
-    traffic = None
-    tp = ROOT / "profiles" / "decode_traffic.json"
-    if tp.exists() and args.workload == "C5":
-        traffic = json.loads(tp.read_text()).get("bytes_per_bit", 0) * n
+    alu_peak, alu_src, dual_peak = alu_peaks(sms, sm_mhz)
+    stats = vd.frame_stats(cfg, n)
+    ops_bit = alu_ops_per_bit(stats.stages, n, S)
+    bits_per_gpu_s = n / world / (ms_step * 1e-3)  # average per GPU over the slowest rank's time
+    alu_achieved = ops_bit * bits_per_gpu_s / 1e12
+    hbm_bytes_bit = B + 1 / 8  # int8 LLR read once + packed output
+    hbm_achieved = hbm_bytes_bit * bits_per_gpu_s / 1e9
+    tb_bit, t_src = kernel_traffic(args.workload if not args.frame else "")
+    traffic = tb_bit * n / world if tb_bit is not None else None
 
     result = None
     if rank == 0:
         cpu = None
         if not args.no_cpu:
-            g, cores, kind, sample, _ = cpu_reference_rate(args.cpu_seconds, code=args.code)
-            cpu = {"value": g, "unit": "Gbps", "cores": cores, "kind": kind, "sample": sample}
+            arm = CpuArm(args.code, target_s=args.cpu_seconds / 3)
+            dt = sorted(arm.time_once() for _ in range(3))[1]
+            cpu = {"value": arm.n / dt / 1e9, "unit": "Gbps", "cores": arm.cores, "kind": arm.kind,
+                   "sample": arm.sample() + " (median of 3)"}
         result = {
             "metric": "decoded info Gbps (K=7 r1/2 soft)" if args.workload in ("C5", "C1") else
                       f"decoded info Gbps (K={args.code[0]} B={args.code[1]} soft)",
@@ -357,21 +501,24 @@ def run_ours(args):
             "warmup": args.warmup,
             "ms_per_step": ms_step,
             "higher_is_better": True,
-            "scaling": "weak",
+            "scaling": "strong",
             "vs_baseline": None,
-            "dtype": "int8 LLR / int32 path metrics" if not t.fast_path() else "int8 LLR / int16x2 path metrics",
-            "data": "synthetic: random message, K=7 encoder, BPSK+AWGN at 3 dB, int8 q=rint(32y), generated in HBM",
+            "dtype": "int8 LLR / int16x2 path metrics" if t.fast_path() else "int8 LLR / int32 path metrics",
+            "data": "synthetic: random message, encoder, BPSK+AWGN at 3 dB, int8 q=rint(32y), generated in HBM",
             "config": {
                 "workload": args.workload_desc if not args.frame else
                             f"{args.workload_desc.split(',')[0]}, frame override f={F} v1={V1} v2={V2} f0={F0}",
-                "info_bits_per_gpu_per_step": n,
-                "frames_per_gpu": nf,
-                "parallelism": f"frame shards x{world} (no collective)",
+                "info_bits_per_step": n,
+                "frames": nf,
+                "parallelism": (f"one stream sharded over {world} GPUs: contiguous word-aligned frame ranges "
+                                f"(vd_partition_frames) + v1/v2 halo, no collective" if world > 1 else "1 GPU"),
                 "l2": (f"inputs ({B} B/bit x {n} bits = {n * B / 2**30:.2f} GiB) exceed L2; no flush needed"
-                       if n * B > 256 << 20 else
+                       if n * B // world > 256 << 20 else
                        f"inputs ({n * B / 2**20:.1f} MiB) fit in L2: steps re-read them warm (latency-bound size)"),
                 "kernel": "fast (register-resident)" if t.fast_path() else "generic (warp per frame)",
-                "ber_check": ber,
+                "bit_errors_vs_sent": errs,
+                "ber_check": errs / n,
+                "identity_vs_1gpu_decode": identity,
             },
             "roofline": {
                 "bound": "alu",
@@ -380,19 +527,25 @@ def run_ours(args):
                 "unit": "Tops",
                 "frac": alu_achieved / alu_peak,
                 "traffic": traffic,
+                "traffic_source": t_src,
                 "ops_per_bit": ops_bit,
                 "peak_source": alu_src,
+                "dual_issue": {"peak": dual_peak, "frac": alu_achieved / dual_peak,
+                               "source": "384 lane-ops/clk/SM (profiles/r01_pipe_probe_ncu.csv pipe rates)"},
                 "hbm": {"achieved": hbm_achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                        "frac": hbm_achieved / peaks["hbm_gbs"], "bytes_per_bit": hbm_bytes / n,
+                        "frac": hbm_achieved / peaks["hbm_gbs"], "bytes_per_bit": hbm_bytes_bit,
                         "peak_source": peak_src},
             },
             "cpu_baseline": cpu,
-            "e2e": {"value": e2e_gbps, "unit": "Gbps", "h2d_bytes_per_step": ne * B,
-                    "d2h_bytes_per_step": ((ne + 31) // 32) * 4, "info_bits_per_step": ne,
+            "e2e": {"value": e2e_gbps, "unit": "Gbps", "h2d_bytes_per_step": ne * B * world,
+                    "d2h_bytes_per_step": ((ne + 31) // 32) * 4 * world, "info_bits_per_step": ne * world,
                     "matches_device_decode": same},
-            "gpu_launches": 3 * args.steps,  # per step: head/tail edge frames (generic) + fast kernel
+            "gpu_launches": int(round(launches * args.steps)),
+            "gpu_launches_per_step_per_rank": launches,
             "clocks": clocks,
         }
+        if weak:
+            result["weak_scaling"] = weak
         print(json.dumps(result))
     if dist:
         dist.barrier()

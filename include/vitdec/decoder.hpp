@@ -66,7 +66,7 @@ DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const Fr
 
 /// Execution options for the native entry point.
 struct ExecOptions {
-  int gpus = 1;                  // frames sharded over devices 0 .. gpus-1
+  int gpus = 0;                  // > 0: frames sharded over devices 0 .. gpus-1; 0: the current device
   std::int64_t chunk_stages = 0; // streaming chunk per device (0 = automatic)
 };
 

@@ -235,12 +235,24 @@ vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n
 vd_status vd_synth_llr_i8_device(const vd_code* code, int64_t n_stages, double sigma, double scale, uint64_t seed,
                                  int8_t* llr_dev, uint32_t* bits_dev, int32_t device, void* stream);
 
+/* Stages [t_begin, t_begin + n_stages) of the same synthetic stream (every
+ * value is a pure function of (seed, stage)): a shard's halo window is
+ * generated on its own device, identical to the whole-stream values. llr_dev
+ * receives stage t at (t - t_begin) * B; bits_dev (t_begin % 32 == 0 only)
+ * the packed message bits of the range; llr_dev may be NULL (bits only). */
+vd_status vd_synth_llr_i8_range_device(const vd_code* code, int64_t t_begin, int64_t n_stages, double sigma,
+                                       double scale, uint64_t seed, int8_t* llr_dev, uint32_t* bits_dev,
+                                       int32_t device, void* stream);
+
 /* Number of bit positions where packed a and b differ over n bits (device). */
 vd_status vd_count_bit_errors_device(const uint32_t* a_dev, const uint32_t* b_dev, int64_t n_bits,
                                      unsigned long long* count_dev, int32_t device, void* stream);
 
 const char* vd_last_error(void);
 const char* vd_version(void);
+/* Kernels this library has launched so far in the process (all devices and
+ * threads): a benchmark reads it around its timed region. */
+uint64_t vd_kernel_launches(void);
 
 #ifdef __cplusplus
 }

@@ -72,6 +72,8 @@ SIGNATURES = {
     "vd_decode_f64": (I32, [P, C.POINTER(VdFrameCfg), P, I64, P, C.POINTER(VdStats), C.POINTER(VdExec)]),
     "vd_serial_decode_f64": (I32, [P, P, I64, P, C.POINTER(VdStats), I32]),
     "vd_synth_llr_i8_device": (I32, [P, I64, DBL, DBL, U64, P, P, I32, P]),
+    "vd_synth_llr_i8_range_device": (I32, [P, I64, I64, DBL, DBL, U64, P, P, I32, P]),
+    "vd_kernel_launches": (U64, []),
     "vd_count_bit_errors_device": (I32, [P, P, I64, P, I32, P]),
     "vd_puncture_validate": (I32, [C.POINTER(VdPuncture)]),
     "vd_depuncture_stages": (I32, [C.POINTER(VdPuncture), I64, C.POINTER(I64)]),

@@ -19,7 +19,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from ._lib import VdPuncture, VdExec, VdFrameCfg, VdStats, check, lib
+from ._lib import VD_EUNSUPPORTED, VdPuncture, VdExec, VdFrameCfg, VdStats, VitdecError, check, lib
 
 __all__ = [
     "CodeSpec",
@@ -164,6 +164,11 @@ class FrameConfig:
     seed: int = 0
 
     def to_c(self) -> VdFrameCfg:
+        # the C-ABI fields are int32: refuse values ctypes would silently truncate
+        for name in ("f", "v1", "v2", "f0"):
+            v = int(getattr(self, name))
+            if not -(1 << 31) <= v < (1 << 31):
+                raise ValueError(f"FrameConfig.{name} = {v} does not fit the decoder's int32 field")
         return VdFrameCfg(int(self.f), int(self.v1), int(self.v2), int(self.f0), int(self.start), 0,
                           int(self.seed) & 0xFFFFFFFFFFFFFFFF)
 
@@ -204,7 +209,15 @@ def _stats(s: VdStats) -> DecodeStats:
     return DecodeStats(int(s.frames), int(s.stages), int(s.tracebacks))
 
 
-def _exec(gpus: int, chunk_stages: int = 0) -> VdExec:
+def _exec(gpus: int, chunk_stages: int = 0, devices=None) -> VdExec:
+    """vd_exec: `devices` (a list of device indices, repeats allowed) shards the
+    frames over those devices; else gpus > 0 -> devices 0 .. gpus-1, 0 -> the
+    current device."""
+    if devices:
+        arr = (C.c_int32 * len(devices))(*[int(d) for d in devices])
+        ex = VdExec(len(devices), C.cast(arr, C.POINTER(C.c_int32)), int(chunk_stages))
+        ex._keep = arr  # the array must outlive the call
+        return ex
     return VdExec(int(gpus) if gpus and gpus > 0 else 0, None, int(chunk_stages))
 
 
@@ -217,7 +230,7 @@ def _check_block(llr: np.ndarray, trellis: Trellis) -> None:
 
 
 def framed_decode_stream(llr_stream: np.ndarray, n: int, trellis: Trellis, cfg: FrameConfig, gpus: int = 0,
-                         chunk_stages: int = 0):
+                         chunk_stages: int = 0, devices=None):
     """Native entry: stage-major stream (int8 or float64, n*B values) ->
     (packed uint32 bits, DecodeStats), through vd_decode_i8 / vd_decode_f64."""
     arr = np.ascontiguousarray(llr_stream)
@@ -226,7 +239,7 @@ def framed_decode_stream(llr_stream: np.ndarray, n: int, trellis: Trellis, cfg: 
     out = np.zeros((n + 31) // 32, np.uint32)
     st = VdStats()
     c = cfg.to_c()
-    ex = _exec(gpus, chunk_stages)
+    ex = _exec(gpus, chunk_stages, devices)
     if arr.dtype == np.int8:
         check(lib().vd_decode_i8(trellis.handle, C.byref(c), arr.ctypes.data, n, out.ctypes.data, C.byref(st),
                                  C.byref(ex)))
@@ -307,6 +320,8 @@ def serial_decode(llr: np.ndarray, trellis: Trellis) -> DecodeOutput:
     n = llr.shape[1]
     stream = _as_stream(llr)
     if stream.dtype == np.int8:
+        if n > 0x7FFFFFFF:  # one frame of n stages: f is an int32 (vd_serial_decode_f64's limit too)
+            raise VitdecError(VD_EUNSUPPORTED, "serial decode limited to 2^31-1 stages")
         packed, st = framed_decode_stream(stream, n, trellis, FrameConfig(f=n), chunk_stages=n)
     else:
         packed = np.zeros((n + 31) // 32, np.uint32)

@@ -7,6 +7,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <condition_variable>
 #include <deque>
 #include <functional>
@@ -497,10 +498,18 @@ vd_status decode_batch_device(const vd_code* code, const vd_frame_cfg* cfg, std:
     lists.insert(lists.end(), kv.second.begin(), kv.second.end());
   }
   const std::size_t bytes = sizeof(std::int64_t) * (2 * nb1 + lists.size()) + sizeof(std::int32_t) * 2 * nb1;
-  // pinned staging (per host thread, grows) so the table upload is a true async copy
-  thread_local unsigned char* pinned = nullptr;
-  thread_local std::size_t pinned_cap = 0;
-  thread_local cudaEvent_t pinned_done = nullptr;  // last upload out of the staging buffer
+  // pinned staging (per host thread and device, grows) so the table upload is
+  // a true async copy; the event is created on the device whose stream records it
+  struct BatchStaging {
+    unsigned char* pinned = nullptr;
+    std::size_t cap = 0;
+    cudaEvent_t done = nullptr;  // last upload out of the staging buffer
+  };
+  thread_local std::map<int, BatchStaging> staging;
+  BatchStaging& bs = staging[dev];
+  unsigned char*& pinned = bs.pinned;
+  std::size_t& pinned_cap = bs.cap;
+  cudaEvent_t& pinned_done = bs.done;
   if (pinned_done) VD_CUDA(cudaEventSynchronize(pinned_done), "batch table staging");
   if (pinned_cap < bytes) {
     if (pinned) cudaFreeHost(pinned);
@@ -843,7 +852,8 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
   // Buffer sizes per device.
   const std::int64_t max_window = std::min<std::int64_t>(chunk_frames * cfg->f + cfg->v1 + cfg->v2, n);
   const std::size_t llr_bytes = sizeof(T) * static_cast<std::size_t>(max_window) * code->b;
-  const std::size_t out_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>((chunk_frames * cfg->f + 31) / 32 + 1);
+  const std::int64_t max_out = std::min<std::int64_t>(chunk_frames * cfg->f, n);  // f >= n: one clipped frame
+  const std::size_t out_bytes = sizeof(std::uint32_t) * static_cast<std::size_t>((max_out + 31) / 32 + 1);
 
   for (int d = 0; d < nd; ++d) {
     if (plan[d].empty()) continue;
@@ -897,13 +907,16 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
     ctx.hout_pending[slot] = false;
     return VD_OK;
   };
-  // Issue: chunk i of every device on that device's stream i % 2. Within a
-  // stream, the H2D of chunk i+2 is ordered after the kernel of chunk i.
-  for (std::size_t i = 0; i < max_chunks; ++i) {
-    for (int d = 0; d < nd; ++d) {
-      if (i >= plan[d].size()) continue;
-      DeviceGuard guard(devices[d]);
-      DevCtx& ctx = tl_ctx.devs[devices[d]];
+  // Issue: one host thread per device (the caller's thread for the first),
+  // so one device's staging copies and waits never hold up another's. Chunk
+  // i of a device goes on its stream i % 2; within a stream the H2D of chunk
+  // i+2 is ordered after the kernel of chunk i. Every worker uses the calling
+  // thread's per-device context (each device is driven by exactly one worker).
+  ThreadCtx& tctx = tl_ctx;
+  auto run_device = [&](int d) -> vd_status {
+    DeviceGuard guard(devices[d]);
+    DevCtx& ctx = tctx.devs[devices[d]];
+    for (std::size_t i = 0; i < plan[d].size(); ++i) {
       const int slot = static_cast<int>(i & 1);
       cudaStream_t s = ctx.st[slot];
       const Chunk c = plan[d][i];
@@ -947,16 +960,53 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
         ctx.pend_bytes[slot] = obytes;
       }
     }
-  }
-  for (int d = 0; d < nd; ++d) {
-    if (plan[d].empty()) continue;
-    DeviceGuard guard(devices[d]);
-    DevCtx& ctx = tl_ctx.devs[devices[d]];
     for (int i = 0; i < 2; ++i) {
       if (vd_status st = drain(ctx, i)) return st;
       VD_CUDA(cudaStreamSynchronize(ctx.st[i]), "decode stream");
       ctx.hin_used[i] = false;
     }
+    return VD_OK;
+  };
+  std::vector<int> active;
+  for (int d = 0; d < nd; ++d) {
+    if (!plan[d].empty()) active.push_back(d);
+  }
+  if (active.size() <= 1) return active.empty() ? VD_OK : run_device(active[0]);
+  // A device listed twice ({0, 0}) gets two chunk lists but one DevCtx: such
+  // entries share a worker, which runs the lists one after the other.
+  std::map<int, std::vector<int>> by_dev;
+  for (int d : active) by_dev[devices[d]].push_back(d);
+  std::vector<vd_status> status(by_dev.size(), VD_OK);
+  std::vector<std::string> msg(by_dev.size());
+  std::vector<std::thread> workers;
+  auto work = [&](std::size_t w, const std::vector<int>& lst) {
+    for (int d : lst) {
+      status[w] = run_device(d);
+      if (status[w] != VD_OK) {
+        msg[w] = g_err;  // thread_local: hand the message to the caller
+        return;
+      }
+    }
+  };
+  std::size_t w = 0;
+  const std::vector<int>* first_list = nullptr;
+  for (auto& kv : by_dev) {
+    if (!first_list) {
+      first_list = &kv.second;
+      ++w;
+      continue;
+    }
+    try {
+      workers.emplace_back(work, w, std::cref(kv.second));
+    } catch (...) {  // no thread: run it on the caller after the others
+      work(w, kv.second);
+    }
+    ++w;
+  }
+  work(0, *first_list);
+  for (auto& th : workers) th.join();
+  for (std::size_t i = 0; i < status.size(); ++i) {
+    if (status[i] != VD_OK) return fail(status[i], msg[i]);
   }
   return VD_OK;
 }
@@ -964,6 +1014,11 @@ vd_status decode_host(const vd_code* code, const vd_frame_cfg* cfg, const T* llr
 }  // namespace
 
 namespace vd {
+namespace {
+std::atomic<unsigned long long> g_launches{0};
+}
+void note_launch(int n) { g_launches.fetch_add(static_cast<unsigned long long>(n), std::memory_order_relaxed); }
+
 cudaError_t retain_async_pool() {
   static std::mutex mu;
   static std::map<int, bool> done;
@@ -997,7 +1052,8 @@ int sm_count() {
 extern "C" {
 
 const char* vd_last_error(void) { return g_err.c_str(); }
-const char* vd_version(void) { return "vitdec_b200 0.1 (sm_100a)"; }
+const char* vd_version(void) { return "vitdec_b200 0.2 (sm_100a)"; }
+uint64_t vd_kernel_launches(void) { return vd::g_launches.load(std::memory_order_relaxed); }
 
 vd_status vd_code_create(int32_t k, int32_t b, const uint32_t* polys, vd_code** out) {
   if (!out) return fail(VD_EINVAL, "null output handle");
@@ -1298,12 +1354,18 @@ vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n
 
 vd_status vd_synth_llr_i8_device(const vd_code* code, int64_t n, double sigma, double scale, uint64_t seed,
                                  int8_t* llr, uint32_t* bits, int32_t device, void* stream) {
-  if (!code || !llr || n < 1) return fail(VD_EINVAL, "bad synth arguments");
+  return vd_synth_llr_i8_range_device(code, 0, n, sigma, scale, seed, llr, bits, device, stream);
+}
+
+vd_status vd_synth_llr_i8_range_device(const vd_code* code, int64_t t_begin, int64_t n, double sigma, double scale,
+                                       uint64_t seed, int8_t* llr, uint32_t* bits, int32_t device, void* stream) {
+  if (!code || (!llr && !bits) || n < 1 || t_begin < 0) return fail(VD_EINVAL, "bad synth arguments");
+  if (bits && (t_begin & 31)) return fail(VD_EINVAL, "message bits need t_begin % 32 == 0");
   if (code->b > 4) return fail(VD_EUNSUPPORTED, "synthetic generator supports B <= 4");
   int dev = 0;
   if (vd_status st = resolve_device(device, &dev)) return st;
   DeviceGuard guard(dev);
-  const cudaError_t e = vd::launch_synth_i8(code->k, code->b, code->polys.data(), n, sigma, scale, seed, llr, bits,
+  const cudaError_t e = vd::launch_synth_i8(code->k, code->b, code->polys.data(), t_begin, n, sigma, scale, seed, llr, bits,
                                             static_cast<cudaStream_t>(stream));
   if (e != cudaSuccess) return cuda_fail(e, "synth kernel");
   return VD_OK;

@@ -186,6 +186,7 @@ cudaError_t launch_depuncture_i8(const DepunctureLaunch& p, cudaStream_t stream)
   const std::int64_t cap = static_cast<std::int64_t>(sm_count()) * 4;
   const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
   depuncture_kernel<<<grid, 256, smem, stream>>>(p);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -37,6 +37,7 @@ cudaError_t launch_head_gather(const std::int8_t* llr, const std::int64_t* blk_s
   if (grid <= 0) return cudaSuccess;
   fast::head_gather_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(llr, blk_stage, nblocks, b, v1, pitch,
                                                                             copy, head);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -1510,6 +1510,7 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream) {
       return ea;
   }
   kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fpl);
+  note_launch();
   e = cudaGetLastError();
   if (fpl.gscratch) {
     const cudaError_t ef = cudaFreeAsync(fpl.gscratch, stream);

@@ -589,6 +589,7 @@ cudaError_t launch_reg(GenericParams gp, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e == cudaSuccess) {
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(gp);
+    note_launch();
     e = cudaGetLastError();
   }
   if (gp.dec_global) {
@@ -658,6 +659,7 @@ cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
   if (e == cudaSuccess) {
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(gp);
+    note_launch();
     e = cudaGetLastError();
   }
   if (gp.dec_global) {

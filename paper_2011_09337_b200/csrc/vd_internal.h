@@ -122,10 +122,16 @@ cudaError_t launch_depuncture_i8(const DepunctureLaunch& p, cudaStream_t stream)
 cudaError_t launch_unpack_i4(const std::uint8_t* in, int nib_off, std::int64_t count, std::int8_t* out,
                              cudaStream_t stream);
 
-cudaError_t launch_synth_i8(int k, int b, const std::uint32_t* polys, std::int64_t n, double sigma, double scale,
-                            std::uint64_t seed, std::int8_t* llr, std::uint32_t* bits, cudaStream_t stream);
+cudaError_t launch_synth_i8(int k, int b, const std::uint32_t* polys, std::int64_t t_begin, std::int64_t n,
+                            double sigma, double scale, std::uint64_t seed, std::int8_t* llr, std::uint32_t* bits,
+                            cudaStream_t stream);
 cudaError_t launch_count_bit_errors(const std::uint32_t* a, const std::uint32_t* b, std::int64_t n_bits,
                                     unsigned long long* count, cudaStream_t stream);
+
+/// Kernel launches issued by this library (every <<<>>> site calls
+/// note_launch); exported as vd_kernel_launches() so benchmarks count the
+/// launches of their timed region instead of assuming them.
+void note_launch(int n = 1);
 
 /// SM count of the current device (cached per device).
 int sm_count();

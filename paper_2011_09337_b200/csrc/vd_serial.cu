@@ -604,6 +604,7 @@ cudaError_t run(SerialParams p, cudaStream_t s) {
   p.endst = reinterpret_cast<std::int32_t*>(q);
   const std::int64_t warpsA = static_cast<std::int64_t>(p.nseg) * p.s;
   if (!launch_cols(p, s)) segment_matrix_kernel<NPL, BT><<<static_cast<unsigned>((warpsA + 3) / 4), 128, 0, s>>>(p);
+  note_launch();
   // B: two-level max-plus scan of the segment matrices. Group products (in
   // parallel), a sequential chain over the groups, then every group's own
   // chain from its start metrics (in parallel).
@@ -626,6 +627,7 @@ cudaError_t run(SerialParams p, cudaStream_t s) {
   segment_map_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
   chain_kernel<<<1, 32, 0, s>>>(p);
   segment_emit_kernel<NPL><<<static_cast<unsigned>((p.nseg + 3) / 4), 128, 0, s>>>(p);
+  note_launch(7);  // group products, 2 chains, forward, map, chain, emit
   cudaError_t e = cudaGetLastError();
   cudaFreeAsync(prod, s);
   const cudaError_t ef = cudaFreeAsync(buf, s);

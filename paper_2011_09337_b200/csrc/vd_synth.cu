@@ -28,18 +28,20 @@ __device__ __forceinline__ std::uint32_t msg_bit(std::uint64_t seed, std::int64_
 constexpr int kStagesPerThread = 8;
 
 __global__ void synth_kernel(int k, int b, std::uint32_t p0, std::uint32_t p1, std::uint32_t p2, std::uint32_t p3,
-                             std::int64_t n, float sigma, float scale, std::uint64_t seed, std::int8_t* __restrict__ llr,
-                             std::uint32_t* __restrict__ bits) {
+                             std::int64_t tb, std::int64_t n, float sigma, float scale, std::uint64_t seed,
+                             std::int8_t* __restrict__ llr, std::uint32_t* __restrict__ bits) {
   const std::uint32_t polys[4] = {p0, p1, p2, p3};
   const std::uint64_t noise_seed = mix_seed(seed, 0xA5A5A5A5ull);
-  const std::int64_t t0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kStagesPerThread;
-  if (t0 >= n) return;
+  // stream stages [tb, tb + n); local index = t - tb
+  const std::int64_t l0 = (static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) * kStagesPerThread;
+  if (l0 >= n) return;
+  const std::int64_t t0 = tb + l0;
   // Encoder register before stage t0: bits t0-1 ... t0-K+1 (newest at the MSB).
   std::uint32_t state = 0;
   for (int i = k - 1; i >= 1; --i) state = (state >> 1) | (msg_bit(seed, t0 - i) << (k - 2));
   for (int j = 0; j < kStagesPerThread; ++j) {
     const std::int64_t t = t0 + j;
-    if (t >= n) break;
+    if (t - tb >= n) break;
     const std::uint32_t u = msg_bit(seed, t);
     const std::uint32_t reg = (u << (k - 1)) | state;
     for (int i = 0; i < b; ++i) {
@@ -52,17 +54,17 @@ __global__ void synth_kernel(int k, int b, std::uint32_t p0, std::uint32_t p1, s
       const float y = (c ? -1.0f : 1.0f) + sigma * z;
       float q = rintf(scale * y);
       q = fminf(fmaxf(q, -127.0f), 127.0f);
-      llr[t * b + i] = static_cast<std::int8_t>(q);
+      if (llr) llr[(t - tb) * b + i] = static_cast<std::int8_t>(q);
     }
     state = (u << (k - 2)) | (state >> 1);
   }
-  if (bits && (t0 & 31) == 0) {
+  if (bits && (l0 & 31) == 0) {
     // the thread whose first stage starts a 32-stage word writes that word
-    const std::int64_t wi = t0 >> 5;
-    std::uint32_t v = msg_word(seed, wi);
-    const std::int64_t rem = n - wi * 32;
+    // (tb % 32 == 0: local and stream words coincide up to the offset)
+    std::uint32_t v = msg_word(seed, t0 >> 5);
+    const std::int64_t rem = n - l0;
     if (rem < 32) v &= (1u << rem) - 1u;
-    bits[wi] = v;
+    bits[l0 >> 5] = v;
   }
 }
 
@@ -83,16 +85,18 @@ __global__ void count_errors_kernel(const std::uint32_t* __restrict__ a, const s
 
 }  // namespace
 
-cudaError_t launch_synth_i8(int k, int b, const std::uint32_t* polys, std::int64_t n, double sigma, double scale,
-                            std::uint64_t seed, std::int8_t* llr, std::uint32_t* bits, cudaStream_t stream) {
+cudaError_t launch_synth_i8(int k, int b, const std::uint32_t* polys, std::int64_t t_begin, std::int64_t n,
+                            double sigma, double scale, std::uint64_t seed, std::int8_t* llr, std::uint32_t* bits,
+                            cudaStream_t stream) {
   if (b > 4) return cudaErrorNotSupported;
   std::uint32_t p[4] = {0, 0, 0, 0};
   for (int i = 0; i < b; ++i) p[i] = polys[i];
   const std::int64_t threads = (n + kStagesPerThread - 1) / kStagesPerThread;
   const std::int64_t blocks = (threads + 255) / 256;
-  synth_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(k, b, p[0], p[1], p[2], p[3], n,
+  synth_kernel<<<static_cast<unsigned>(blocks), 256, 0, stream>>>(k, b, p[0], p[1], p[2], p[3], t_begin, n,
                                                                   static_cast<float>(sigma), static_cast<float>(scale),
                                                                   seed, llr, bits);
+  note_launch();
   return cudaGetLastError();
 }
 
@@ -101,6 +105,7 @@ cudaError_t launch_count_bit_errors(const std::uint32_t* a, const std::uint32_t*
   cudaError_t e = cudaMemsetAsync(count, 0, sizeof(unsigned long long), stream);
   if (e != cudaSuccess) return e;
   count_errors_kernel<<<sm_count() * 4, 256, 0, stream>>>(a, b, n_bits, count);
+  note_launch();
   return cudaGetLastError();
 }
 

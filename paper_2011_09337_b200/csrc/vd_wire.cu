@@ -77,6 +77,7 @@ cudaError_t launch_unpack_i4(const std::uint8_t* in, int nib_off, std::int64_t c
   const std::int64_t grid = std::min<std::int64_t>((groups + 255) / 256, cap);
   unpack_i4_kernel<<<static_cast<unsigned>(grid), 256, 0, stream>>>(reinterpret_cast<const std::uint32_t*>(in),
                                                                      nbytes, nib_off & 1, count, out);
+  note_launch();
   return cudaGetLastError();
 }
 

@@ -56,11 +56,13 @@ void check_block(const LlrBlock& llr, const Trellis& trellis) {
   if (llr.rows() != trellis.outputs_per_bit()) throw std::invalid_argument("llr row count must equal B");
 }
 
+// VITDEC_GPUS=N shards the drop-in decode over devices 0 .. N-1; unset (or
+// <= 0) decodes on the calling thread's current device (vd_exec num_devices 0).
 int env_gpus() {
   const char* v = std::getenv("VITDEC_GPUS");
-  if (!v || !*v) return 1;
+  if (!v || !*v) return 0;
   const int g = std::atoi(v);
-  return g > 0 ? g : 1;
+  return g > 0 ? g : 0;
 }
 
 // True when every value is an integer in [-127, 127]: the block is then
@@ -296,7 +298,7 @@ DecodeStats framed_decode(const std::int8_t* llr, std::int64_t n_stages, const T
   const vd_frame_cfg c = to_c(cfg);
   vd_stats st{};
   vd_exec ex{};
-  ex.num_devices = exec.gpus > 0 ? exec.gpus : 1;
+  ex.num_devices = exec.gpus > 0 ? exec.gpus : 0;
   ex.chunk_stages = exec.chunk_stages;
   check(vd_decode_i8(trellis.native(), &c, llr, n_stages, packed_out, &st, &ex));
   return from_c(st);
@@ -313,7 +315,7 @@ DecodeStats framed_decode_punctured(const std::int8_t* punctured, std::int64_t n
   }
   vd_stats st{};
   vd_exec ex{};
-  ex.num_devices = exec.gpus > 0 ? exec.gpus : 1;
+  ex.num_devices = exec.gpus > 0 ? exec.gpus : 0;
   ex.chunk_stages = exec.chunk_stages;
   check(vd_decode_punctured_i8(trellis.native(), &c, &pc, punctured, n_punctured, packed_out, &st, &ex));
   return from_c(st);

@@ -65,6 +65,14 @@ def synth_llr_i8(trellis: Trellis, n: int, sigma: float, scale: float, seed: int
                                        _stream(stream)))
 
 
+def synth_llr_i8_range(trellis: Trellis, t_begin: int, n: int, sigma: float, scale: float, seed: int, llr,
+                       bits=None, device: int = -1, stream=None) -> None:
+    """Stages [t_begin, t_begin + n) of the synth_llr_i8 stream (a shard's window)."""
+    check(lib().vd_synth_llr_i8_range_device(trellis.handle, int(t_begin), int(n), float(sigma), float(scale),
+                                             int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(llr), _ptr(bits), int(device),
+                                             _stream(stream)))
+
+
 def count_bit_errors(a, b, n_bits: int, count, device: int = -1, stream=None) -> None:
     check(lib().vd_count_bit_errors_device(_ptr(a), _ptr(b), int(n_bits), _ptr(count), int(device),
                                            _stream(stream)))

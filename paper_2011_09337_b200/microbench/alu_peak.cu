@@ -15,6 +15,8 @@
 //   8 VIMNMX + IMAD        (pipe co-issue probe)
 //   9 SHFL.BFLY            (__shfl_xor_sync)
 //  10 VIMNMX with predicate outputs consumed by SEL (decision extraction)
+//  11 the fast kernel's packed ACS: s2 = VIADD.16x2(sO, T'), n = VIADDMNMX.S16x2(sE, T, s2)
+//     (1:1 fmaheavy : alu; 3 lane-ops per instruction, 2 frames per register)
 #include <cuda_runtime.h>
 
 #include <cstdint>
@@ -62,6 +64,9 @@ __global__ void __launch_bounds__(256) mb_kernel(std::uint32_t seed, int iters, 
           y[i] = y[i] * m + x[(i + 1) & 7];
         } else if constexpr (OP == 9) {
           x[i] = __shfl_xor_sync(0xffffffffu, x[i], 1 + (i & 3)) + y[i];
+        } else if constexpr (OP == 11) {
+          const std::uint32_t s2 = __vadd2(x[(i + 1) & 7], y[i]);
+          x[i] = __viaddmax_s16x2(x[i], y[(i + 3) & 7], s2);
         } else if constexpr (OP == 10) {
           bool hi, lo;
           x[i] = __vibmax_s16x2(x[i], y[i], &hi, &lo);
@@ -114,8 +119,8 @@ extern "C" {
 /// Instructions of the measured kind issued per thread per inner iteration
 /// (x8 chains x4 unroll), by op code.
 int vdmb_instr_per_iter(int op) {
-  static const int k[] = {32, 32, 96, 32, 32, 32, 32, 64, 64, 32, 32};
-  return (op >= 0 && op <= 10) ? k[op] : 0;
+  static const int k[] = {32, 32, 96, 32, 32, 32, 32, 64, 64, 32, 32, 64};
+  return (op >= 0 && op <= 11) ? k[op] : 0;
 }
 
 /// Runs op over blocks x threads for iters iterations. Returns the elapsed
@@ -133,6 +138,7 @@ int vdmb_run(int op, int blocks, int threads, int iters, float* ms, double* avg_
     case 8: return run<8>(blocks, threads, iters, ms, avg_cycles);
     case 9: return run<9>(blocks, threads, iters, ms, avg_cycles);
     case 10: return run<10>(blocks, threads, iters, ms, avg_cycles);
+    case 11: return run<11>(blocks, threads, iters, ms, avg_cycles);
     default: return -1;
   }
 }

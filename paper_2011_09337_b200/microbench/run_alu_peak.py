@@ -18,7 +18,9 @@ from pathlib import Path
 HERE = Path(__file__).resolve().parent
 ROOT = HERE.parents[1]
 NAMES = ["VIADD.16x2", "VIMNMX.S16x2", "VIADD.16x2+VIADDMNMX (ACS mix)", "IADD3", "IMAD", "PRMT", "LOP3",
-         "VIADD.16x2+IMAD", "VIMNMX+IMAD", "SHFL.BFLY(+IADD)", "VIMNMX(pred)+SEL"]
+         "VIADD.16x2+IMAD", "VIMNMX+IMAD", "SHFL.BFLY(+IADD)", "VIMNMX(pred)+SEL",
+         "ACS pair VIADD.16x2+VIADDMNMX (1:1, the fast kernel's)"]
+ACS = NAMES[11]
 
 
 def main(out=ROOT / "profiles" / "alu_peak.json"):
@@ -39,16 +41,24 @@ def main(out=ROOT / "profiles" / "alu_peak.json"):
         mhz = cyc.value / (ms.value * 1e3)
         res[name] = {"warp_instr_per_sm_clk": per_sm_clk, "ms": ms.value, "sm_mhz_seen": mhz}
         print(f"{name:34s} {per_sm_clk:6.3f} warp-instr/SM/clk   ({ms.value:.2f} ms, {mhz:.0f} MHz)")
-    acs = res[NAMES[2]]
-    lane_ops_per_clk = acs["warp_instr_per_sm_clk"] * 32 * 2  # packed 16x2: 2 lane-ops per instruction
+    acs = res[ACS]
+    # the packed ACS pair makes one new register (2 frames x 1 state, 2 adds +
+    # 1 compare-select each = 6 lane-ops) per 2 instructions: 3 lane-ops per
+    # warp-lane instruction
+    lane_ops_per_clk = acs["warp_instr_per_sm_clk"] * 32 * 3
     tops_seen = lane_ops_per_clk * sms * acs["sm_mhz_seen"] * 1e6 / 1e12
-    tops_max = lane_ops_per_clk * sms * 1965e6 / 1e12
+    dual = 4 * 32 * 3  # 1 warp-instr / clk / SMSP with the fmaheavy and alu pipes each at 0.5
     summary = {
-        "source": "microbenchmark paper_2011_09337_b200/microbench/alu_peak.cu (VIADD.16x2+VIADDMNMX.S16x2 mix)",
+        "source": "microbenchmark paper_2011_09337_b200/microbench/alu_peak.cu op 11 (the fast kernel's "
+                  "VIADD.16x2 -> VIADDMNMX.S16x2 ACS pair), run by run_alu_peak.py on the bench box",
+        "acs_warp_instr_per_sm_clk": acs["warp_instr_per_sm_clk"],
         "lane_ops_per_sm_clk": lane_ops_per_clk,
+        "dual_issue_lane_ops_per_sm_clk": dual,
         "sms": sms,
+        "sm_mhz_seen": acs["sm_mhz_seen"],
         "tops": tops_seen,
-        "tops_at_1965mhz": tops_max,
+        "tops_at_1965mhz": lane_ops_per_clk * sms * 1965e6 / 1e12,
+        "dual_issue_tops_at_1965mhz": dual * sms * 1965e6 / 1e12,
         "ops": res,
     }
     out.parent.mkdir(parents=True, exist_ok=True)
