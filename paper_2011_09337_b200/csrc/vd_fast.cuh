@@ -252,7 +252,9 @@ struct FastParams {
   // IMAD multiplier 2 read from the parameter bank: ptxas cannot constant-fold
   // it, so the decision arithmetic written as mad_u32 stays on the FMA pipe
   // instead of becoming ALU-pipe LEA / IADD3.
-  std::uint32_t two;
+  // (field order matters: two and m1 adjacent made ptxas load them as one
+  // 64-bit uniform pair and copy them into registers in every block)
+  std::uint32_t two, pad0, m1;
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -284,6 +286,9 @@ __device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t 
 #define VD_FMA_PAIRS 6      // butterflies per stage with FMA-pipe decision words (rest: ALU form)
 #endif
 constexpr int kFmaPairs = VD_FMA_PAIRS;
+#ifndef VD_NEG_FMA
+#define VD_NEG_FMA 1        // negated branch tables as IMAD (param-bank -1) on the FMA pipe (C5 +0.5 %, C4 +0.9 %)
+#endif
 #ifndef VD_FAST_TB
 #define VD_FAST_TB 1        // serial-traceback fast path (+6 %)
 #endif
@@ -360,6 +365,7 @@ struct FrameState {
   std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : 3];
   std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
   std::uint32_t two_p;                // 2 from the parameter bank (not constant-folded by ptxas)
+  std::uint32_t m1_p;                 // -1 from the parameter bank
   std::uint32_t corr;                 // pending renormalisation (BASE - ref per half)
 };
 
@@ -402,7 +408,7 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
 #pragma unroll
     for (int x = 0; x < GEO::NT; ++x) {
       // T[x ^ XM] = -T[x]
-      PT[k][x ^ XM] = OFFB - PT[k][x];
+      PT[k][x ^ XM] = VD_NEG_FMA ? mad_u32(PT[k][x], st.m1_p, OFFB) : OFFB - PT[k][x];
     }
   }
 }
@@ -689,6 +695,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
   }
   st.two_p = fp.two;
+  st.m1_p = fp.m1;
   st.corr = 0u;
 #pragma unroll
   for (int i = 0; i < R; ++i) st.sig[i] = BASE;
@@ -1298,6 +1305,7 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   fp.head_pitch = p.head_pitch;
   fp.p = p;
   fp.two = 2u;
+  fp.m1 = 0xffffffffu;
   fp.L = p.f + p.v1 + p.v2;
   fp.nblk = (fp.L + GEO::LB - 1) / GEO::LB;
   fp.step = p.f0 > 0 ? p.f0 : p.f;

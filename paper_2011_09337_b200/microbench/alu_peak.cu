@@ -25,7 +25,7 @@ namespace {
 
 template <int OP>
 __global__ void __launch_bounds__(256) mb_kernel(std::uint32_t seed, int iters, std::uint32_t* out,
-                                                 unsigned long long* cycles) {
+                                                 unsigned long long* span) {
   std::uint32_t x[8], y[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
@@ -81,18 +81,31 @@ __global__ void __launch_bounds__(256) mb_kernel(std::uint32_t seed, int iters, 
 #pragma unroll
   for (int i = 0; i < 8; ++i) acc ^= x[i] + y[i];
   out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
-  if (threadIdx.x == 0) atomicAdd(cycles, static_cast<unsigned long long>(c1 - c0));
+  // per-SM active span: earliest start and latest end of any block on this SM
+  // (clock64 is a per-SM counter; blocks of one SM need not overlap fully)
+  if (threadIdx.x == 0) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    atomicMin(span + 2 * smid, static_cast<unsigned long long>(c0));
+    atomicMax(span + 2 * smid + 1, static_cast<unsigned long long>(c1));
+  }
+}
+
+__global__ void span_init(unsigned long long* span, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) span[i] = (i & 1) ? 0ull : ~0ull;
 }
 
 template <int OP>
 cudaError_t run(int blocks, int threads, int iters, float* ms, double* avg_cycles) {
   std::uint32_t* out = nullptr;
   unsigned long long* cyc = nullptr;
+  const int nspan = 2 * 1024;  // smid < 1024
   cudaMalloc(&out, sizeof(std::uint32_t) * blocks * threads);
-  cudaMalloc(&cyc, sizeof(unsigned long long));
-  cudaMemset(cyc, 0, sizeof(unsigned long long));
+  cudaMalloc(&cyc, sizeof(unsigned long long) * nspan);
+  span_init<<<(nspan + 255) / 256, 256>>>(cyc, nspan);
   mb_kernel<OP><<<blocks, threads>>>(0x12345u, 16, out, cyc);  // warm-up
-  cudaMemset(cyc, 0, sizeof(unsigned long long));
+  span_init<<<(nspan + 255) / 256, 256>>>(cyc, nspan);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
@@ -101,9 +114,17 @@ cudaError_t run(int blocks, int threads, int iters, float* ms, double* avg_cycle
   cudaEventRecord(e1);
   cudaError_t err = cudaEventSynchronize(e1);
   cudaEventElapsedTime(ms, e0, e1);
-  unsigned long long c = 0;
-  cudaMemcpy(&c, cyc, sizeof(c), cudaMemcpyDeviceToHost);
-  *avg_cycles = static_cast<double>(c) / blocks;
+  static unsigned long long h[2 * 1024];
+  cudaMemcpy(h, cyc, sizeof(unsigned long long) * nspan, cudaMemcpyDeviceToHost);
+  double sum = 0.0;
+  int used = 0;
+  for (int i = 0; i < nspan / 2; ++i) {
+    if (h[2 * i + 1] != 0ull) {
+      sum += static_cast<double>(h[2 * i + 1] - h[2 * i]);
+      ++used;
+    }
+  }
+  *avg_cycles = used ? sum / used : 0.0;  // mean per-SM active span (cycles)
   cudaFree(out);
   cudaFree(cyc);
   cudaEventDestroy(e0);
@@ -124,7 +145,8 @@ int vdmb_instr_per_iter(int op) {
 }
 
 /// Runs op over blocks x threads for iters iterations. Returns the elapsed
-/// milliseconds and the mean per-block clock64 cycles of the timed loop.
+/// milliseconds and the mean per-SM active span (clock64 cycles from the
+/// first block start to the last block end on that SM) of the timed loop.
 int vdmb_run(int op, int blocks, int threads, int iters, float* ms, double* avg_cycles) {
   switch (op) {
     case 0: return run<0>(blocks, threads, iters, ms, avg_cycles);

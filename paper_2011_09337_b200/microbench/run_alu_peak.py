@@ -28,7 +28,7 @@ def main(out=ROOT / "profiles" / "alu_peak.json"):
     lib.vdmb_run.argtypes = [C.c_int, C.c_int, C.c_int, C.c_int, C.POINTER(C.c_float), C.POINTER(C.c_double)]
     lib.vdmb_instr_per_iter.argtypes = [C.c_int]
     sms = lib.vdmb_sm_count()
-    blocks, threads, iters = sms * 8, 256, 4000
+    blocks, threads, iters = sms * 8, 256, 40000
     res = {}
     for op, name in enumerate(NAMES):
         ms, cyc = C.c_float(), C.c_double()

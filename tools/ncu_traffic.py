@@ -53,7 +53,8 @@ def main(workloads):
     import os
 
     out = Path(os.environ.get("VITDEC_TRAFFIC_OUT", ROOT / "profiles" / "decode_traffic.json"))
-    head = subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True, text=True, cwd=ROOT).stdout
+    head = os.environ.get("VITDEC_TREE") or subprocess.run(["git", "rev-parse", "--short", "HEAD"], capture_output=True,
+                                                           text=True, cwd=ROOT).stdout
     d = json.loads(out.read_text()) if out.exists() else {}
     d.setdefault("workloads", {})
     d.pop("bytes_per_bit", None)  # round-1 single-figure format
