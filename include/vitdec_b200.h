@@ -20,7 +20,7 @@
  *    exact std::invalid_argument message the reference throws.
  *  - All entry points are re-entrant and thread-safe (the reference calls
  *    framed_decode concurrently from BER-sweep worker threads,
- *    reference berlab.cpp:260-284): no mutable global state except the
+ *    reference berlab.cpp:63-88): no mutable global state except the
  *    per-thread error string and a per-(thread, device) stream cache.
  *  - There is no CPU fallback: without a usable CUDA device every decode
  *    entry point returns VD_ECUDA.
@@ -225,6 +225,13 @@ vd_status vd_unpack_i4_device(const uint8_t* llr4_dev, int64_t count, int8_t* ll
 /* serial_decode (reference decoder.cpp:101-129): one frame, no overlap. */
 vd_status vd_serial_decode_f64(const vd_code* code, const double* llr, int64_t n_stages, uint32_t* out_packed,
                                vd_stats* stats, int32_t device);
+
+/* Real-valued depuncture on host buffers (the drop-in vitdec::depuncture,
+ * reference decoder.cpp:131-163): n_stages from vd_depuncture_stages;
+ * llr_out receives n_stages * B doubles, stage-major, 0.0 at punctured
+ * positions. Runs on the current device (no CPU fallback). */
+vd_status vd_depuncture_f64(const vd_puncture* pattern, const double* punctured, int64_t n_punctured,
+                            double* llr_out);
 
 /* ---- synthetic input (bench / streaming tests; not reference parity data) - */
 

@@ -127,7 +127,7 @@ int vdref_serial_decode_f64(int k, int b, const std::uint32_t* polys, const doub
   });
 }
 
-/// The throughput-bench data recipe (reference berlab.cpp:335-339): n info
+/// The throughput-bench data recipe (reference berlab.cpp:138-142): n info
 /// bits from random_bits(n, mix_seed(seed,1)), encoded, BPSK, AWGN at the
 /// base-rate sigma for ebn0_db with seed mix_seed(seed,2). Writes the n*B
 /// received stream and the n sent bits.
@@ -145,7 +145,7 @@ int vdref_gen_bench_block(int k, int b, const std::uint32_t* polys, std::int64_t
   });
 }
 
-/// One block of the BER-sweep recipe (reference berlab.cpp:263-277),
+/// One block of the BER-sweep recipe (reference berlab.cpp:66-80),
 /// unpunctured: block_seed as computed by run_ber_sweep.
 int vdref_gen_sweep_block(int k, int b, const std::uint32_t* polys, std::int64_t n, double sigma,
                           std::uint64_t block_seed, double* rx_out, std::uint8_t* sent_out) {

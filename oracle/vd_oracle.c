@@ -439,14 +439,14 @@ static int gen_block(int k, int b, const uint32_t* polys, int64_t n, double sigm
 
 int vdo_gen_bench_block(int k, int b, const uint32_t* polys, int64_t n, double ebn0_db, uint64_t seed, double* rx,
                         uint8_t* sent) {
-  /* berlab.cpp:335-339: base-rate sigma, seeds mix_seed(seed,1/2). */
+  /* berlab.cpp:138-142: base-rate sigma, seeds mix_seed(seed,1/2). */
   return gen_block(k, b, polys, n, vdo_sigma_from_ebn0(ebn0_db, 1.0 / b), vdo_mix_seed(seed, 1),
                    vdo_mix_seed(seed, 2), rx, sent);
 }
 
 int vdo_gen_sweep_block(int k, int b, const uint32_t* polys, int64_t n, double sigma, uint64_t block_seed,
                         double* rx, uint8_t* sent) {
-  /* berlab.cpp:265-274 (identity puncture pattern) */
+  /* berlab.cpp:68-79 (identity puncture pattern) */
   return gen_block(k, b, polys, n, sigma, vdo_mix_seed(block_seed, 1), vdo_mix_seed(block_seed, 2), rx, sent);
 }
 

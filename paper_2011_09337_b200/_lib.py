@@ -78,6 +78,7 @@ SIGNATURES = {
     "vd_puncture_validate": (I32, [C.POINTER(VdPuncture)]),
     "vd_depuncture_stages": (I32, [C.POINTER(VdPuncture), I64, C.POINTER(I64)]),
     "vd_depuncture_i8_device": (I32, [C.POINTER(VdPuncture), P, I64, P, I32, P]),
+    "vd_depuncture_f64": (I32, [C.POINTER(VdPuncture), P, I64, P]),
     "vd_decode_punctured_i8": (I32, [P, C.POINTER(VdFrameCfg), C.POINTER(VdPuncture), P, I64, P, C.POINTER(VdStats),
                                      C.POINTER(VdExec)]),
     "vd_decode_punctured_i8_device": (I32, [P, C.POINTER(VdFrameCfg), C.POINTER(VdPuncture), P, I64, P, P,

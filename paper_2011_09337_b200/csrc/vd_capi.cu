@@ -1260,6 +1260,38 @@ vd_status vd_depuncture_stages(const vd_puncture* pattern, int64_t n_punctured, 
   return punct_stages(pp, n_punctured, n_stages);
 }
 
+vd_status vd_depuncture_f64(const vd_puncture* pattern, const double* punctured, int64_t n_punctured,
+                            double* llr_out) {
+  PunctPlan pp;
+  if (vd_status st = make_punct(pattern, &pp)) return st;
+  std::int64_t n = 0;
+  if (vd_status st = punct_stages(pp, n_punctured, &n)) return st;
+  if (n == 0) return VD_OK;
+  if (!punctured || !llr_out) return fail(VD_EINVAL, "null buffer");
+  int dev = 0;
+  if (vd_status st = resolve_device(-1, &dev)) return st;
+  DeviceGuard guard(dev);
+  DevCtx& ctx = tl_ctx.devs[dev];
+  if (!ctx.st[0]) VD_CUDA(cudaStreamCreateWithFlags(&ctx.st[0], cudaStreamNonBlocking), "cudaStreamCreate");
+  cudaStream_t s = ctx.st[0];
+  VD_CUDA(vd::retain_async_pool(), "memory pool");
+  double* din = nullptr;
+  double* dout = nullptr;
+  const std::size_t in_bytes = sizeof(double) * static_cast<std::size_t>(std::max<std::int64_t>(n_punctured, 1));
+  const std::size_t out_bytes = sizeof(double) * static_cast<std::size_t>(n) * pp.b;
+  VD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&din), in_bytes, s), "cudaMallocAsync(depuncture in)");
+  VD_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&dout), out_bytes, s), "cudaMallocAsync(depuncture out)");
+  cudaError_t e = cudaMemcpyAsync(din, punctured, sizeof(double) * n_punctured, cudaMemcpyHostToDevice, s);
+  if (e == cudaSuccess) e = vd::launch_depuncture_f64(din, n, pp.b, pp.period, pp.kept, pp.rank.data(), dout, s);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(llr_out, dout, out_bytes, cudaMemcpyDeviceToHost, s);
+  cudaFreeAsync(din, s);
+  cudaFreeAsync(dout, s);
+  const cudaError_t es = cudaStreamSynchronize(s);
+  if (e != cudaSuccess) return cuda_fail(e, "depuncture");
+  if (es != cudaSuccess) return cuda_fail(es, "depuncture");
+  return VD_OK;
+}
+
 vd_status vd_depuncture_i8_device(const vd_puncture* pattern, const int8_t* punctured_dev, int64_t n_punctured,
                                   int8_t* llr_dev, int32_t device, void* stream) {
   PunctPlan pp;

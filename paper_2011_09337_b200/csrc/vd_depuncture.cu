@@ -20,6 +20,7 @@
 // (grid-stride over tiles).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <climits>
 #include <cstdint>
 
@@ -186,6 +187,36 @@ cudaError_t launch_depuncture_i8(const DepunctureLaunch& p, cudaStream_t stream)
   const std::int64_t cap = static_cast<std::int64_t>(sm_count()) * 4;
   const unsigned grid = static_cast<unsigned>(tiles < cap ? tiles : cap);
   depuncture_kernel<<<grid, 256, smem, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+namespace {
+struct RankTable {
+  std::int16_t r[kMaxPunctureCells];
+};
+
+__global__ void depuncture_f64_kernel(const double* __restrict__ in, std::int64_t count, int b, int period, int kept,
+                                      RankTable rt, double* __restrict__ out) {
+  for (std::int64_t e = static_cast<std::int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < count;
+       e += static_cast<std::int64_t>(gridDim.x) * blockDim.x) {
+    const std::int64_t t = e / b;
+    const int row = static_cast<int>(e - t * b);
+    const int cell = static_cast<int>(t % period) * b + row;
+    const int r = rt.r[cell];
+    out[e] = r < 0 ? 0.0 : in[(t / period) * kept + r];
+  }
+}
+}  // namespace
+
+cudaError_t launch_depuncture_f64(const double* in, std::int64_t n_stages, int b, int period, int kept,
+                                  const std::int16_t* rank, double* out, cudaStream_t stream) {
+  RankTable rt{};
+  for (int i = 0; i < period * b && i < kMaxPunctureCells; ++i) rt.r[i] = rank[i];
+  const std::int64_t count = n_stages * b;
+  const std::int64_t blocks = std::min<std::int64_t>((count + 255) / 256, static_cast<std::int64_t>(sm_count()) * 8);
+  depuncture_f64_kernel<<<static_cast<unsigned>(blocks > 0 ? blocks : 1), 256, 0, stream>>>(in, count, b, period, kept,
+                                                                                         rt, out);
   note_launch();
   return cudaGetLastError();
 }

@@ -116,6 +116,11 @@ struct DepunctureLaunch {
   std::int16_t rank[kMaxPunctureCells] = {};
 };
 cudaError_t launch_depuncture_i8(const DepunctureLaunch& p, cudaStream_t stream);
+/// Real-valued depuncture (the drop-in vitdec::depuncture on LlrBlock
+/// doubles): one thread per output element, out[t * b + row] =
+/// in[(t / period) * kept + rank[(t % period) * b + row]] or 0.
+cudaError_t launch_depuncture_f64(const double* in, std::int64_t n_stages, int b, int period, int kept,
+                                  const std::int16_t* rank, double* out, cudaStream_t stream);
 
 /// 4-bit wire format: widen `count` signed nibbles (element i in nibble
 /// nib_off + i of `in`, low nibble first) to int8 at `out` (8-byte aligned).

@@ -213,35 +213,19 @@ void acs_stage(const Eigen::ArrayXd& sigma_prev, const double* stage_table, cons
   }
 }
 
-// reference decoder.cpp:131-163, without calling PuncturePattern's
-// out-of-line members (those live in the transmitter harness).
+// reference decoder.cpp:131-163 (depuncture): validation and the stage count
+// through the C-ABI (vd_depuncture_stages, same messages), the gather itself
+// on the device (vd_depuncture_f64); LlrBlock is column-major B x N, i.e. the
+// stage-major stream the kernel writes.
 LlrBlock depuncture(const Eigen::Ref<const Eigen::ArrayXd>& punctured, const PuncturePattern& p) {
-  if (p.b < 1 || p.period < 1 || static_cast<int>(p.mask.size()) != p.b * p.period) {
-    throw std::invalid_argument("puncture mask shape mismatch");
-  }
-  std::vector<int> kept(static_cast<std::size_t>(p.period), 0);
-  int per_period = 0;
-  for (int col = 0; col < p.period; ++col) {
-    for (int row = 0; row < p.b; ++row) kept[col] += p.at(row, col);
-    if (kept[col] == 0) throw std::invalid_argument("puncture mask drops an entire stage");
-    per_period += kept[col];
-  }
-  Eigen::Index rem = punctured.size();
-  Eigen::Index stages = (rem / per_period) * p.period;
-  rem %= per_period;
-  for (int col = 0; rem > 0; ++col) {
-    if (col >= p.period || rem < kept[col]) throw std::invalid_argument("punctured length inconsistent with pattern");
-    rem -= kept[col];
-    ++stages;
-  }
+  if (static_cast<int>(p.mask.size()) != p.b * p.period) throw std::invalid_argument("puncture mask shape mismatch");
+  const vd_puncture pc{p.b, p.period, p.mask.data()};
+  std::int64_t stages = 0;
+  check(vd_depuncture_stages(&pc, punctured.size(), &stages));
   LlrBlock block = LlrBlock::Zero(p.b, stages);
-  Eigen::Index idx = 0;
-  for (Eigen::Index t = 0; t < stages; ++t) {
-    const int col = static_cast<int>(t % p.period);
-    for (int row = 0; row < p.b; ++row) {
-      if (p.at(row, col)) block(row, t) = punctured[idx++];
-    }
-  }
+  if (stages == 0) return block;
+  const Eigen::ArrayXd in = punctured;  // contiguous copy (Ref may be strided)
+  check(vd_depuncture_f64(&pc, in.data(), in.size(), block.data()));
   return block;
 }
 

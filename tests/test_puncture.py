@@ -213,3 +213,38 @@ def test_punctured_noiseless_round_trip_large():
     packed, n2, _ = vd.framed_decode_punctured(punct, vd.PuncturePattern.parse(rows), t, vd.FrameConfig(256, 24, 48))
     assert n2 == n
     assert np.array_equal(packed, bits.cpu().numpy().view(np.uint32))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["r23", "r34"])
+def test_drop_in_depuncture_f64_matches_reference(name):
+    """vd_depuncture_f64 (the device gather behind the drop-in
+    vitdec::depuncture) on real-valued streams == the reference's depuncture."""
+    ref = oracle.reference()
+    if ref is None:
+        pytest.skip("reference library not built (oracle/_ref)")
+    import ctypes as C
+
+    from paper_2011_09337_b200._lib import VdPuncture, check, lib
+
+    rows = _rows(name)
+    b, period, mask = oracle._mask_arr(rows)
+    m = np.ascontiguousarray(mask, np.uint8)
+    pc = VdPuncture(b, period, m.ctypes.data)
+    rng = np.random.default_rng(11)
+    kept = int(m.sum())
+    for n_p in (1, kept, kept * 5 + 2, 100_003 // kept * kept):
+        d = rng.normal(size=n_p)
+        st = C.c_int64()
+        out = np.zeros(2 * n_p + 8, np.float64)
+        status = ref.fn("depuncture")(name.encode(), d.ctypes.data, d.size, out.ctypes.data, out.size, C.addressof(st))
+        n_stages = C.c_int64()
+        ours_status = lib().vd_depuncture_stages(C.byref(pc), n_p, C.byref(n_stages))
+        if status != 0:
+            assert ours_status != 0
+            continue
+        check(ours_status)
+        assert n_stages.value == st.value
+        got = np.zeros(n_stages.value * b, np.float64)
+        check(lib().vd_depuncture_f64(C.byref(pc), d.ctypes.data, n_p, got.ctypes.data))
+        assert np.array_equal(got, out[:n_stages.value * b]), (name, n_p)
