@@ -38,3 +38,35 @@ def test_dropin_api_workers_and_native_overload():
     r = subprocess.run([str(WORKERS_BIN)], capture_output=True, text=True, timeout=600, cwd="/tmp")
     print(r.stdout[-2000:], r.stderr[-2000:])
     assert r.returncode == 0 and "OK" in r.stdout, r.stdout + r.stderr
+
+
+ACC_BIN = ROOT / "oracle" / "_ref" / "dropin_acceptance"
+
+
+@pytest.mark.skipif(not ACC_BIN.exists(), reason="drop-in acceptance binary not built (make -C oracle dropin)")
+def test_reference_acceptance_suite_on_gpu_decoder():
+    """The reference's acceptance suite (proj/tests/acceptance.cpp:57-338),
+    compiled unmodified against include/vitdec and linked with this library:
+    every framed_decode / serial_decode it makes (oracle equivalence, ML
+    oracle, noiseless recovery at r1/2 2/3 3/4, the Table I / III BER-gap
+    cells at 1e7 bits per point, traceback start, scaling invariance, soft vs
+    hard) runs on the GPU. Criteria 1-8 and 10 must PASS. Criterion 9 times
+    the CPU decoder's `workers` scaling (9a: speedup >= 0.5 W per host
+    thread count) — on the GPU the decode is one device pass and `workers`
+    only parallelises the host-side conversion, so 9 is reported, not gated."""
+    import os
+
+    r = subprocess.run([str(ACC_BIN)], capture_output=True, text=True, timeout=2400, cwd="/tmp")
+    out_dir = ROOT / "gpurun_out"
+    if out_dir.exists() or os.environ.get("GRAFT_REPO_ROOT"):
+        out_dir.mkdir(exist_ok=True)
+        (out_dir / "dropin_acceptance.txt").write_text(r.stdout + "\n--- stderr ---\n" + r.stderr[-4000:])
+    print(r.stdout)
+    res = {}
+    for line in r.stdout.splitlines():
+        if line.startswith("[PASS] criterion") or line.startswith("[FAIL] criterion"):
+            num = int(line.split("criterion")[1].split(":")[0])
+            res[num] = line
+    for c in (1, 2, 3, 4, 5, 6, 7, 8, 10):
+        assert c in res and res[c].startswith("[PASS]"), res.get(c, f"criterion {c} missing\n{r.stderr[-2000:]}")
+    assert 9 in res
