@@ -8,8 +8,8 @@ CPU oracle.
   soft values quantised to int8 (scale 32); the GPU batched decode must make
   exactly the oracle's bit errors, point by point.
 * Monte-Carlo: an independent large-sample GPU curve (device-side synthetic
-  AWGN, 2^22 bits per point) must agree with the oracle's curve within
-  binomial tolerance, and both must fall monotonically with Eb/N0.
+  AWGN, 2^24 bits per point) must agree with the oracle's curve (reference
+  data chain, 2^20 bits per point) within binomial tolerance.
 """
 import numpy as np
 import pytest
@@ -56,17 +56,25 @@ def test_ber_curve_error_counts_match_oracle(f, v2):
         prev = e_gpu
 
 
+MC_BLOCKS = 128  # oracle side: 128 x 8192 = 2^20 bits per point
+
+
 def test_large_sample_curve_within_monte_carlo_tolerance():
-    """GPU curve at 2^22 bits/point (device AWGN) vs the oracle's curve at
-    BLOCKS*BLOCK_BITS bits/point (reference data chain): |p1 - p2| within
-    4 sigma of the pooled binomial estimate (+ a 15 % relative allowance
-    for the int8 quantiser and the generators' differing noise samples)."""
+    """GPU curve at 2^24 bits/point (device AWGN) vs the oracle's curve at
+    2^20 bits/point (reference data chain, run_ber_sweep block recipe): |p1 -
+    p2| within 4 sigma of the pooled binomial estimate (+ 3 % relative for
+    the generators' differing float / double noise samples; both sides use
+    the same int8 quantiser). Points where the oracle sees < 20 errors get a
+    one-sided bound instead."""
+    from concurrent.futures import ThreadPoolExecutor
+    import os
+
     import torch
 
     port = oracle.port()
     t = vd.build_trellis(vd.CodeSpec(*K7))
     cfg = vd.FrameConfig(256, 20, 42)
-    n = 1 << 22
+    n = 1 << 24
     from paper_2011_09337_b200.device import count_bit_errors, decode_i8_device, synth_llr_i8
 
     llr = torch.empty(n * 2, dtype=torch.int8, device="cuda")
@@ -81,16 +89,20 @@ def test_large_sample_curve_within_monte_carlo_tolerance():
         count_bit_errors(out, bits, n, cnt)
         torch.cuda.synchronize()
         p_gpu = int(cnt.item()) / n
-        blocks, sents = _point_blocks(port, ebn0, p)
-        e = 0
-        for q, s in zip(blocks, sents):
-            b, _, _ = port.framed_decode(*K7, q, BLOCK_BITS, 256, 20, 42)
-            e += int(np.count_nonzero(b != s))
-        m = BLOCKS * BLOCK_BITS
+        sigma_p = port.sigma_from_ebn0(ebn0, 0.5)
+
+        def one(blk):
+            rx, sent = port.gen_sweep_block(*K7, BLOCK_BITS, sigma_p, port.mix_seed(SEED + 1, p * 0x100000 + blk))
+            b, _, _ = port.framed_decode(*K7, oracle.quantize(rx, 32.0), BLOCK_BITS, 256, 20, 42)
+            return int(np.count_nonzero(b != sent))
+
+        with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
+            e = sum(ex.map(one, range(MC_BLOCKS)))
+        m = MC_BLOCKS * BLOCK_BITS
         p_ora = e / m
         if e < 20:  # too few oracle errors for a two-sample check: one-sided bound
             assert p_gpu < 30.0 / m, (ebn0, p_gpu, p_ora)
             continue
         pooled = (p_gpu * n + e) / (n + m)
-        tol = 4.0 * np.sqrt(pooled * (1 - pooled) * (1.0 / n + 1.0 / m)) + 0.15 * pooled
+        tol = 4.0 * np.sqrt(pooled * (1 - pooled) * (1.0 / n + 1.0 / m)) + 0.03 * pooled
         assert abs(p_gpu - p_ora) <= tol, (ebn0, p_gpu, p_ora, tol)
