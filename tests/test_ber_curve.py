@@ -57,15 +57,26 @@ def test_ber_curve_error_counts_match_oracle(f, v2):
 
 
 MC_BLOCKS = 128  # oracle side: 128 x 8192 = 2^20 bits per point
+EVENT_GAP = 32   # decoder bit errors closer than this belong to one error event
+
+
+def _events(err_positions):
+    """Viterbi errors come in bursts (one wrong path segment = several bit
+    errors), so bits are not independent trials; error EVENTS are."""
+    e = np.asarray(err_positions)
+    if e.size == 0:
+        return 0
+    return int(1 + np.count_nonzero(np.diff(e) > EVENT_GAP))
 
 
 def test_large_sample_curve_within_monte_carlo_tolerance():
     """GPU curve at 2^24 bits/point (device AWGN) vs the oracle's curve at
-    2^20 bits/point (reference data chain, run_ber_sweep block recipe): |p1 -
-    p2| within 4 sigma of the pooled binomial estimate (+ 3 % relative for
-    the generators' differing float / double noise samples; both sides use
-    the same int8 quantiser). Points where the oracle sees < 20 errors get a
-    one-sided bound instead."""
+    2^20 bits/point (reference data chain, run_ber_sweep block recipe), both
+    int8-quantised: the error-EVENT rates (bursts of bit errors within 32
+    bits count once; events, unlike bit errors, are near-independent) agree
+    within 4 sigma of the pooled binomial estimate + 5 % relative, and so do
+    the BERs within the same test inflated by the measured burst length.
+    Points with < 10 oracle events get a one-sided bound instead."""
     from concurrent.futures import ThreadPoolExecutor
     import os
 
@@ -75,34 +86,40 @@ def test_large_sample_curve_within_monte_carlo_tolerance():
     t = vd.build_trellis(vd.CodeSpec(*K7))
     cfg = vd.FrameConfig(256, 20, 42)
     n = 1 << 24
-    from paper_2011_09337_b200.device import count_bit_errors, decode_i8_device, synth_llr_i8
+    from paper_2011_09337_b200.device import decode_i8_device, synth_llr_i8
 
     llr = torch.empty(n * 2, dtype=torch.int8, device="cuda")
     bits = torch.empty((n + 31) // 32, dtype=torch.int32, device="cuda")
     out = torch.empty((n + 31) // 32 + 1, dtype=torch.int32, device="cuda")
-    cnt = torch.zeros(1, dtype=torch.int64, device="cuda")
     for p, ebn0 in enumerate(EBN0[:5]):
         sigma = port.sigma_from_ebn0(ebn0, 0.5)
         synth_llr_i8(t, n, sigma, 32.0, 77 + p, llr, bits)
         decode_i8_device(t, cfg, n, llr, 0, 0, (n + 255) // 256, out, 0)
-        cnt.zero_()
-        count_bit_errors(out, bits, n, cnt)
         torch.cuda.synchronize()
-        p_gpu = int(cnt.item()) / n
+        diff = (out[: n // 32] ^ bits[: n // 32]).cpu().numpy().view(np.uint32)
+        pos = np.flatnonzero(np.unpackbits(diff.view(np.uint8), bitorder="little"))
+        p_gpu, ev_gpu = pos.size / n, _events(pos)
         sigma_p = port.sigma_from_ebn0(ebn0, 0.5)
 
         def one(blk):
             rx, sent = port.gen_sweep_block(*K7, BLOCK_BITS, sigma_p, port.mix_seed(SEED + 1, p * 0x100000 + blk))
             b, _, _ = port.framed_decode(*K7, oracle.quantize(rx, 32.0), BLOCK_BITS, 256, 20, 42)
-            return int(np.count_nonzero(b != sent))
+            w = np.flatnonzero(b != sent)
+            return w.size, _events(w)
 
         with ThreadPoolExecutor(os.cpu_count() or 1) as ex:
-            e = sum(ex.map(one, range(MC_BLOCKS)))
+            res = list(ex.map(one, range(MC_BLOCKS)))
+        e, ev_ora = sum(r[0] for r in res), sum(r[1] for r in res)
         m = MC_BLOCKS * BLOCK_BITS
         p_ora = e / m
-        if e < 20:  # too few oracle errors for a two-sample check: one-sided bound
-            assert p_gpu < 30.0 / m, (ebn0, p_gpu, p_ora)
+        if ev_ora < 10:  # too few oracle events for a two-sample check: one-sided bound
+            assert ev_gpu / n < 25.0 / m, (ebn0, p_gpu, p_ora, ev_gpu, ev_ora)
             continue
-        pooled = (p_gpu * n + e) / (n + m)
-        tol = 4.0 * np.sqrt(pooled * (1 - pooled) * (1.0 / n + 1.0 / m)) + 0.03 * pooled
-        assert abs(p_gpu - p_ora) <= tol, (ebn0, p_gpu, p_ora, tol)
+        q_gpu, q_ora = ev_gpu / n, ev_ora / m
+        pooled = (ev_gpu + ev_ora) / (n + m)
+        tol = 4.0 * np.sqrt(pooled * (1 - pooled) * (1.0 / n + 1.0 / m)) + 0.05 * pooled
+        assert abs(q_gpu - q_ora) <= tol, ("event rate", ebn0, q_gpu, q_ora, tol)
+        burst = (pos.size + e) / max(ev_gpu + ev_ora, 1)  # mean bit errors per event
+        pooled_b = (pos.size + e) / (n + m)
+        tol_b = 4.0 * np.sqrt(burst * pooled_b * (1.0 / n + 1.0 / m)) + 0.05 * pooled_b
+        assert abs(p_gpu - p_ora) <= tol_b, ("ber", ebn0, p_gpu, p_ora, tol_b)
