@@ -110,7 +110,7 @@ std::int64_t align_unit(int f) {
 }
 
 vd_status check_gpu_envelope(const vd_code* code) {
-  if (code->k > 12) return fail(VD_EUNSUPPORTED, "GPU decoder supports K <= 12 (reference allows 16)");
+  if (code->k > vd::kMaxK) return fail(VD_EUNSUPPORTED, "GPU decoder supports K <= 16");
   if (code->b > 8) return fail(VD_EUNSUPPORTED, "GPU decoder supports B <= 8");
   return VD_OK;
 }

@@ -672,10 +672,12 @@ cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
 }  // namespace
 
 cudaError_t launch_generic_i8(const DecodeLaunch& p, cudaStream_t stream) {
+  if (p.k > kMaxGenericK) return launch_bigk_i8(p, stream);  // CTA-per-frame path (vd_bigk.cu)
   return launch_generic<std::int8_t, std::int32_t>(p, stream);
 }
 
 cudaError_t launch_generic_f64(const DecodeLaunch& p, cudaStream_t stream) {
+  if (p.k > kMaxGenericK) return launch_bigk_f64(p, stream);
   return launch_generic<double, double>(p, stream);
 }
 

@@ -71,10 +71,16 @@ __device__ __forceinline__ FrameRef resolve_frame(const DecodeLaunch& p, std::in
 }
 #endif
 
-/// Generic sm_100a kernel (any K in [2, 12], B in [2, 8]); int8 LLRs with
-/// int32 metrics or double LLRs with double metrics.
+/// Generic sm_100a kernels (any K in [2, 16], B in [2, 8]); int8 LLRs with
+/// int32 metrics or double LLRs with double metrics. K <= kMaxGenericK: warp
+/// per frame (vd_generic.cu); larger K: CTA per frame with the path metrics in
+/// a per-CTA global (L2) scratch (vd_bigk.cu, launch_bigk_*).
+constexpr int kMaxGenericK = 12;
+constexpr int kMaxK = 16;  // reference trellis.cpp:44
 cudaError_t launch_generic_i8(const DecodeLaunch& p, cudaStream_t stream);
 cudaError_t launch_generic_f64(const DecodeLaunch& p, cudaStream_t stream);
+cudaError_t launch_bigk_i8(const DecodeLaunch& p, cudaStream_t stream);
+cudaError_t launch_bigk_f64(const DecodeLaunch& p, cudaStream_t stream);
 
 /// Stages a fast-kernel window may read past its end (rounding to 4-stage
 /// blocks + the two-block LLR prefetch); callers building padded copies or
