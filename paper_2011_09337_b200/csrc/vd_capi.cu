@@ -11,6 +11,7 @@
 #include <condition_variable>
 #include <deque>
 #include <functional>
+#include <initializer_list>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -147,6 +148,28 @@ vd_status make_punct(const vd_puncture* pat, PunctPlan* pp) {
     pp->srank[col + 1] = pp->kept;
   }
   return VD_OK;
+}
+
+// Patterns with a fused-depuncture fast-kernel instantiation (vd_fast.cuh
+// PunctR23 / PunctR34): 23 = "11;10", 34 = "110;101"; 0 = none.
+int punct_pattern_id(const PunctPlan& pp) {
+  if (pp.b != 2) return 0;
+  auto is = [&](int period, std::initializer_list<int> kept_cells) {
+    if (pp.period != period) return false;
+    std::vector<int> want(static_cast<std::size_t>(period) * 2, -1);
+    int r = 0;
+    for (int q = 0; q < period * 2; ++q) {
+      const bool k = std::find(kept_cells.begin(), kept_cells.end(), q) != kept_cells.end();
+      if (k) want[q] = r++;
+    }
+    for (int q = 0; q < period * 2; ++q) {
+      if ((pp.rank[q] >= 0) != (want[q] >= 0)) return false;
+    }
+    return true;
+  };
+  if (is(2, {0, 1, 2})) return 23;     // col0 rows 0,1; col1 row 0
+  if (is(3, {0, 1, 2, 5})) return 34;  // col0 rows 0,1; col1 row 0; col2 row 1
+  return 0;
 }
 
 // Stage count of a punctured stream (decoder.cpp:141-152).
@@ -1343,9 +1366,69 @@ vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg*
   if (vd_status st = resolve_device(device, &dev)) return st;
   DeviceGuard guard(dev);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const std::int64_t nf = num_frames(cfg, n);
+  // Fused depuncture (vd_fast.cuh Punct): the fast kernel stages the
+  // punctured stream straight into its shared-memory LLR ring; the few edge
+  // frames it does not take are decoded from dense copies of their windows.
+  // VITDEC_PUNCT_FUSED=0 selects the separate depuncture pass (A/B).
+  const int pid = punct_pattern_id(pp);
+  const char* env_fused = std::getenv("VITDEC_PUNCT_FUSED");
+  const bool want_fused = pid != 0 && (!env_fused || std::atoi(env_fused) != 0) &&
+                          (reinterpret_cast<std::uintptr_t>(punctured_dev) & 3u) == 0 && cfg->f0 == 0;
+  if (want_fused && check_gpu_envelope(code) == VD_OK) {
+    vd::DecodeLaunch p;
+    p.k = code->k;
+    p.b = code->b;
+    p.s = code->s;
+    p.f = cfg->f;
+    p.v1 = cfg->v1;
+    p.v2 = cfg->v2;
+    p.f0 = cfg->f0;
+    p.start = cfg->start;
+    p.seed = cfg->seed;
+    p.n = n;
+    p.frame_begin = 0;
+    p.frame_end = nf;
+    p.llr = punctured_dev;
+    p.llr_stage0 = 0;
+    p.out = out_dev;
+    for (int i = 0; i < code->b && i < 8; ++i) p.polys[i] = code->polys[i];
+    p.complement_paired = code->complement_paired;
+    std::int64_t mi0 = 0, mi1 = 0;
+    if (vd::launch_fast_punct_i8(p, pid, nullptr, nullptr, &mi0, &mi1) && mi1 > mi0) {
+      const std::uint32_t* in_out = nullptr;
+      if (vd_status st = device_table(code, dev, &in_out)) return st;
+      p.in_out = in_out;
+      // edge frames first (their zeroing of shared output words must precede
+      // the fused kernel's writes), each from a dense copy of its window
+      if (mi0 > 0) {
+        const std::int64_t t1 = std::min<std::int64_t>(mi0 * cfg->f + cfg->v2 + vd::kPfSlackStages, n);
+        if (vd_status st = launch_depuncture(pp, punctured_dev, 0, t1, llr_scratch_dev, s)) return st;
+        if (vd_status st = decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, 0, 0, mi0, out_dev, 0, nullptr,
+                                                      dev, stream))
+          return st;
+      }
+      if (mi1 < nf) {
+        const std::int64_t t0 = mi1 * cfg->f - cfg->v1;  // a period multiple: f and v1 are
+        if (vd_status st = launch_depuncture(pp, punctured_dev + pp.off(t0), t0, n - t0, llr_scratch_dev, s))
+          return st;
+        const std::int64_t ow = (mi1 * cfg->f) / 32 * 32;
+        if (vd_status st = decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, t0, mi1, nf, out_dev + ow / 32, ow,
+                                                      nullptr, dev, stream))
+          return st;
+      }
+      // interior frames: zero their own words (minus the edge-shared ones), then the fused kernel
+      const std::int64_t w0 = (mi0 * cfg->f + 31) / 32;
+      const std::int64_t w1 = mi1 < nf ? (mi1 * cfg->f) / 32 : (n + 31) / 32;
+      if (w1 > w0) VD_CUDA(cudaMemsetAsync(out_dev + w0, 0, sizeof(std::uint32_t) * (w1 - w0), s), "zero output");
+      cudaError_t e = cudaSuccess;
+      if (!vd::launch_fast_punct_i8(p, pid, s, &e, &mi0, &mi1)) return fail(VD_ECUDA, "fused depuncture plan changed");
+      if (e != cudaSuccess) return cuda_fail(e, "fused depuncture decode");
+      return VD_OK;
+    }
+  }
   if (vd_status st = launch_depuncture(pp, punctured_dev, 0, n, llr_scratch_dev, s)) return st;
-  return decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, 0, 0, num_frames(cfg, n), out_dev, 0, nullptr,
-                                    dev, stream);
+  return decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, 0, 0, nf, out_dev, 0, nullptr, dev, stream);
 }
 
 vd_status vd_decode_i4(const vd_code* code, const vd_frame_cfg* cfg, const uint8_t* llr4, int64_t n, uint32_t* out,

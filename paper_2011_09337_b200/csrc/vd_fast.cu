@@ -10,6 +10,8 @@ namespace fast {
 bool try_group_k7(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe);
 bool try_group_k9(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe);
 bool try_group_k568(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe);
+bool try_punct_k7(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
+                  std::int64_t* mi1);
 
 __global__ void head_gather_kernel(const std::int8_t* __restrict__ llr, const std::int64_t* __restrict__ blk_stage,
                                    int nblocks, int b, int v1, std::int64_t pitch, std::int64_t copy,
@@ -47,6 +49,11 @@ bool fast_path_supported(const DecodeLaunch& p) {
   cudaError_t unused = cudaSuccess;
   return try_group_k7(p, nullptr, &unused, true) || try_group_k9(p, nullptr, &unused, true) ||
          try_group_k568(p, nullptr, &unused, true);
+}
+
+bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err,
+                          std::int64_t* mi0, std::int64_t* mi1) {
+  return fast::try_punct_k7(p, pattern, stream, err, mi0, mi1);
 }
 
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream) {

@@ -85,6 +85,66 @@ using Code2 = CodeB<K_, 2, P0, P1>;
 template <int K_, std::uint32_t P0, std::uint32_t P1, std::uint32_t P2>
 using Code3 = CodeB<K_, 3, P0, P1, P2>;
 
+/// Puncture pattern of a B = 2 mother code for the fused-depuncture kernel
+/// (reference PuncturePattern, codec.hpp:13-33, codec.cpp:57-71): period P
+/// stages, KEPT bit (col * 2 + row) set when LLR (row, col) is transmitted
+/// (the reference's column-major mask[col * b + row] order). The kernel
+/// re-inserts the punctured zeros while it stages the LLR stream into shared
+/// memory (reference depuncture, decoder.cpp:131-163), one lane per 12 stages
+/// of a frame: every task starts at a stage that is a multiple of P (frames
+/// are period-aligned, decoder.cpp:14-19), so the byte gather is a
+/// compile-time PRMT pattern plus a runtime byte alignment.
+template <int P_, std::uint32_t KEPT_>
+struct Punct {
+  static constexpr bool kActive = true;
+  static constexpr int P = P_;
+  static constexpr std::uint32_t KEPT = KEPT_;
+  static constexpr int kTaskStages = 12;  // stages per fill task (6 output words)
+  static_assert(kTaskStages % P == 0, "a fill task must cover whole periods");
+  static constexpr bool kept(int col, int row) { return ((KEPT >> (col * 2 + row)) & 1u) != 0; }
+  static constexpr int kept_per_period() {
+    int k = 0;
+    for (int c = 0; c < P; ++c) k += kept(c, 0) + kept(c, 1);
+    return k;
+  }
+  static constexpr int task_bytes() { return kept_per_period() * (kTaskStages / P); }
+  /// Source byte (relative to the task's first transmitted byte) of output
+  /// byte j of output word i (stage 2i + j/2, row j%2), or -1 if punctured.
+  static constexpr int src(int i, int j) {
+    const int t = 2 * i + j / 2, row = j % 2;
+    if (!kept(t % P, row)) return -1;
+    int n = 0;
+    for (int q = 0; q < 2 * t + row; ++q) n += kept((q / 2) % P, q % 2);
+    return n;
+  }
+  static constexpr int lo_src(int i) {
+    int m = 1 << 20;
+    for (int j = 0; j < 4; ++j) m = (src(i, j) >= 0 && src(i, j) < m) ? src(i, j) : m;
+    return m;
+  }
+  /// PRMT over (u[lo_src / 4], u[lo_src / 4 + 1]) and the byte keep-mask.
+  static constexpr std::uint32_t sel(int i) {
+    std::uint32_t s = 0;
+    const int a = (lo_src(i) / 4) * 4;
+    for (int j = 0; j < 4; ++j) s |= static_cast<std::uint32_t>(src(i, j) >= 0 ? src(i, j) - a : 0) << (4 * j);
+    return s;
+  }
+  static constexpr std::uint32_t mask(int i) {
+    std::uint32_t m = 0;
+    for (int j = 0; j < 4; ++j) m |= (src(i, j) >= 0 ? 0xffu : 0u) << (8 * j);
+    return m;
+  }
+};
+struct NoPunct {
+  static constexpr bool kActive = false;
+  static constexpr int P = 1;
+};
+using PunctR23 = Punct<2, 0x07>;  // "11;10"  (reference PuncturePattern::named("r23"))
+using PunctR34 = Punct<3, 0x27>;  // "110;101" (named("r34"))
+static_assert(PunctR23::task_bytes() == 18 && PunctR34::task_bytes() == 16, "pattern tables");
+static_assert(PunctR23::sel(1) == 0x0543u && PunctR23::mask(1) == 0x00ffffffu, "r2/3 gather");
+static_assert(PunctR34::mask(1) == 0xffffff00u && PunctR34::mask(2) == 0xff0000ffu, "r3/4 gather");
+
 template <class C, int R_>
 struct Geo {
   static constexpr int M = C::kK - 1;
@@ -230,6 +290,7 @@ struct FastParams {
   int warps_per_cta;
   int smem_per_warp;      // bytes (per-warp area, after the CTA header)
   int dec_off, x_off, ss_off;  // byte offsets of the regions inside a warp's area
+  int stg_off;                 // fused depuncture: LLR staging ring (2 chunks x FPW frames x 12 words)
   // Survivor store split: decisions of stages
   // [t_first, t_split) live in tensor memory (tcols columns per warp, 32 TMEM
   // lanes = the warp's lanes), stages [s_base, L) in shared memory rows
@@ -269,6 +330,14 @@ __device__ __forceinline__ std::uint32_t ldg_pinned(const std::uint32_t* p) {
   std::uint32_t v;
   asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
   return v;
+}
+
+// Fused-depuncture staging: 8-byte shared-memory load / store (shared-space address).
+__device__ __forceinline__ void lds_v2(std::uint32_t saddr, std::uint32_t* v) {
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "r"(saddr));
+}
+__device__ __forceinline__ void sts_v2(std::uint32_t saddr, std::uint32_t a, std::uint32_t b) {
+  asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr), "r"(a), "r"(b) : "memory");
 }
 
 // a * b + c as an IMAD on the FMA pipe (b is an opaque register, so ptxas
@@ -471,9 +540,10 @@ __device__ __forceinline__ void store_dec(const BlockCtx& bc, int t, std::uint32
 // whose pending stores all go to shared memory / tensor memory / global rows;
 // MODE 3 blocks lie entirely in the v1 warm-up (ACS only: no decision words,
 // no stores).
-template <class C, class GEO, int MODE, bool TM, bool GL, int BUF, class RecFn>
+template <class C, class GEO, int MODE, bool TM, bool GL, int BUF, class PN, class RecFn>
 __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const BlockCtx& bc, int& tprev,
-                                          const std::uint32_t* pfA, const std::uint32_t* pfB, RecFn&& rec) {
+                                          const std::uint32_t* pfA, const std::uint32_t* pfB, std::uint32_t sA,
+                                          RecFn&& rec) {
   constexpr int LB = GEO::LB, R = GEO::R, WPB = GEO::WPB;
   constexpr std::uint32_t XM = C::kXM;
   // ---- branch-metric tables for the LB stages of this block (both frames) ---
@@ -496,10 +566,18 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   // (plan() / the head copies / the batch tables guarantee it), so the
   // prefetch never needs clamping; the over-read values are never consumed
   // past stage L-1.
+  if constexpr (PN::kActive) {
+    // fused depuncture: the block's words come from the warp's staging ring
+    // (frame A at sA, frame B one 48-byte frame row later)
+    static_assert(WPB == 2, "fused depuncture stages B = 2 streams");
+    lds_v2(sA, st.llr[BUF][0]);
+    lds_v2(sA + 48u, st.llr[BUF][1]);
+  } else {
 #pragma unroll
-  for (int i = 0; i < WPB; ++i) {
-    st.llr[BUF][0][i] = ldg_pinned(pfA + i);
-    st.llr[BUF][1][i] = ldg_pinned(pfB + i);
+    for (int i = 0; i < WPB; ++i) {
+      st.llr[BUF][0][i] = ldg_pinned(pfA + i);
+      st.llr[BUF][1][i] = ldg_pinned(pfB + i);
+    }
   }
   std::uint32_t tw[4];
 #pragma unroll
@@ -567,7 +645,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
   if constexpr (MODE != 0) tprev = blk * LB + LB - 1;
 }
 
-template <class C, int R, bool TM, bool GL>
+template <class C, int R, bool TM, bool GL, class PN = NoPunct>
 __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const FastParams fp) {
   using GEO = Geo<C, R>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, r = GEO::r, g = GEO::g;
@@ -663,8 +741,68 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
                 : static_cast<const std::int8_t*>(p.llr) + (sl.ws - p.llr_stage0) * B;
     return reinterpret_cast<const std::uint32_t*>(b8);
   };
-  const std::uint32_t* llrA = llr_of(slA);
-  const std::uint32_t* llrB = llr_of(slB);
+  const std::uint32_t* llrA = PN::kActive ? nullptr : llr_of(slA);
+  const std::uint32_t* llrB = PN::kActive ? nullptr : llr_of(slB);
+
+  // ---- fused depuncture: LLR staging ring ----------------------------------
+  // Chunks of 24 stages of the warp's FPW frames are depunctured into a
+  // 2-chunk ring in shared memory ([chunk & 1][frame slot][12 words]); lane
+  // 2q + h fills 12 stages (6 words) of frame slot q. Chunk c + 1 is loaded
+  // during the blocks of chunk c (global loads issued at block 6c, gathered
+  // and stored at block 6c + 2) and first read by the prefetch of block 6c + 4.
+  constexpr std::uint32_t kChunkBytes = static_cast<std::uint32_t>(GEO::FPW) * 48u;
+  std::uint32_t stg_s = 0, rbuf = 0;
+  int rpos = 2, rc = 0, nch = 0;  // prefetch cursor: block b + 2 = chunk rc, block rpos of it
+  const unsigned char* tptr = nullptr;  // this lane's fill task: first transmitted byte of chunk 0
+  bool tvalid = false;
+  std::uint32_t raw[6] = {0u, 0u, 0u, 0u, 0u, 0u};
+  std::uint32_t ralign = 0;
+  (void)stg_s;
+  (void)rbuf;
+  (void)raw;
+  auto fill_issue = [&](int c) {
+    if constexpr (PN::kActive) {
+      const unsigned char* a = tptr + static_cast<std::int64_t>(c) * (2 * PN::task_bytes());
+      ralign = static_cast<std::uint32_t>(reinterpret_cast<std::uintptr_t>(a) & 3u);
+      const std::uint32_t* w = reinterpret_cast<const std::uint32_t*>(a - ralign);
+#pragma unroll
+      for (int j = 0; j < 6; ++j) raw[j] = tvalid ? ldg_pinned(w + j) : 0u;
+    }
+  };
+  auto fill_finish = [&](int c) {
+    if constexpr (PN::kActive) {
+      std::uint32_t u[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) u[j] = __funnelshift_r(raw[j], raw[j + 1], 8u * ralign);
+      std::uint32_t o[6];
+#pragma unroll
+      for (int i = 0; i < 6; ++i) {
+        const int a = PN::lo_src(i) / 4;
+        o[i] = prmt(u[a], u[a + 1 < 5 ? a + 1 : 4], PN::sel(i)) & PN::mask(i);
+      }
+      if (tvalid) {
+        const std::uint32_t s = stg_s + ((c & 1) ? kChunkBytes : 0u) + static_cast<std::uint32_t>(lane >> 1) * 48u +
+                                static_cast<std::uint32_t>(lane & 1) * 24u;
+        sts_v2(s, o[0], o[1]);
+        sts_v2(s + 8u, o[2], o[3]);
+        sts_v2(s + 16u, o[4], o[5]);
+      }
+    }
+  };
+  if constexpr (PN::kActive) {
+    stg_s = static_cast<std::uint32_t>(__cvta_generic_to_shared(wbase + fp.stg_off));
+    const int ft = lane >> 1;
+    tvalid = ft < GEO::FPW;
+    bool vt = tvalid && mbase + ft < fp.mi1;
+    const Slot slT = frame_slot(mbase + ft, vt);  // empty slots read some interior window
+    // frames are period-aligned: window start ws is a multiple of P
+    tptr = static_cast<const unsigned char*>(p.llr) + (slT.ws / PN::P) * PN::kept_per_period() +
+           (lane & 1) * PN::task_bytes();
+    nch = (fp.nblk + 1) / 6 + 1;  // chunks read: blocks 0 .. nblk + 1
+    fill_issue(0);
+    fill_finish(0);
+    __syncwarp();
+  }
 
   FrameState<GEO> st;
   // Per-phase flip constants for this lane (lane part of the branch index).
@@ -703,18 +841,27 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
   for (int i = 0; i < R; ++i) st.wv[1][i] = 0u;
   std::int32_t subA = 0, subB = 0;  // accumulated renormalisation (ref - BASE) per half
 
+  if constexpr (PN::kActive) {
+    const std::uint32_t s0 = stg_s + static_cast<std::uint32_t>(2 * grp) * 48u;
 #pragma unroll
-  for (int b = 0; b < 2; ++b) {
+    for (int b = 0; b < 2; ++b) {
+      lds_v2(s0 + 8u * b, st.llr[b][0]);
+      lds_v2(s0 + 8u * b + 48u, st.llr[b][1]);
+    }
+  } else {
 #pragma unroll
-    for (int i = 0; i < WPB; ++i) {
-      st.llr[b][0][i] = __ldg(llrA + b * WPB + i);
-      st.llr[b][1][i] = __ldg(llrB + b * WPB + i);
+    for (int b = 0; b < 2; ++b) {
+#pragma unroll
+      for (int i = 0; i < WPB; ++i) {
+        st.llr[b][0][i] = __ldg(llrA + b * WPB + i);
+        st.llr[b][1][i] = __ldg(llrB + b * WPB + i);
+      }
     }
   }
   // Prefetch pointers: block b + 2 is requested right after block b has
   // built its tables (two blocks of latency cover).
-  const std::uint32_t* pfA = llrA + 2 * WPB;
-  const std::uint32_t* pfB = llrB + 2 * WPB;
+  const std::uint32_t* pfA = PN::kActive ? nullptr : llrA + 2 * WPB;
+  const std::uint32_t* pfB = PN::kActive ? nullptr : llrB + 2 * WPB;
 
   int next_sub = 0;
   // subframes whose traceback starts from the stored max state
@@ -858,9 +1005,23 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
   // fixed body (per-block mode tests had cost ~40 instructions per block pair).
   auto one_block_mode = [&](int blk, auto mode_tag, auto buf_tag) {
     constexpr int MD = decltype(mode_tag)::value, BUF = decltype(buf_tag)::value;
-    run_block<C, GEO, MD, TM, GL, BUF>(st, blk, bc, tprev, pfA, pfB, rec);
-    pfA += WPB;
-    pfB += WPB;
+    if constexpr (PN::kActive) {
+      const std::uint32_t sA = stg_s + rbuf + static_cast<std::uint32_t>(2 * grp) * 48u + static_cast<std::uint32_t>(rpos) * 8u;
+      run_block<C, GEO, MD, TM, GL, BUF, PN>(st, blk, bc, tprev, pfA, pfB, sA, rec);
+      if (rc + 1 < nch) {
+        if (rpos == 2) fill_issue(rc + 1);
+        if (rpos == 4) fill_finish(rc + 1);
+      }
+      if (++rpos == 6) {
+        rpos = 0;
+        rbuf ^= kChunkBytes;
+        ++rc;
+      }
+    } else {
+      run_block<C, GEO, MD, TM, GL, BUF, PN>(st, blk, bc, tprev, pfA, pfB, 0u, rec);
+      pfA += WPB;
+      pfB += WPB;
+    }
     block_end(blk, buf_tag);
   };
   auto run_mode = [&](auto mode_tag, int& blk, int end) {
@@ -1297,9 +1458,10 @@ struct Plan {
   bool tm, gl;
 };
 
-template <class C, int R>
+template <class C, int R, class PN = NoPunct>
 bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   using GEO = Geo<C, R>;
+  if (PN::kActive && (GEO::B != 2 || pad_head || p.nblocks > 0 || p.llr_stage0 != 0 || p.sigma)) return false;
   FastParams fp{};
   fp.llr_head = p.llr_head;
   fp.head_pitch = p.head_pitch;
@@ -1325,8 +1487,10 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
     if (p.sigma) return false;
   } else {
   // stages read per frame: the window rounded up to whole blocks, plus the
-  // two-block prefetch overrun
-  const std::int64_t span = static_cast<std::int64_t>(fp.nblk) * GEO::LB + 2 * GEO::LB;
+  // two-block prefetch overrun; fused depuncture: whole 24-stage chunks of
+  // blocks 0 .. nblk + 1, plus the fill's 6-word read slack (<= 24 stages)
+  const std::int64_t span = PN::kActive ? static_cast<std::int64_t>((fp.nblk + 1) / 6 + 1) * 24 + 24
+                                        : static_cast<std::int64_t>(fp.nblk) * GEO::LB + 2 * GEO::LB;
   std::int64_t lo = pad_head ? p.frame_begin : (p.v1 + p.f - 1) / p.f;  // first m with m*f >= v1 (or padded head)
   std::int64_t hi_excl = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // m*f + f + v2 <= n
   // the caller guarantees LLRs up to the window end of the last launched frame
@@ -1341,13 +1505,14 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   fp.safe_stage = fp.mi0 * p.f - p.v1;
   }
   const int x_bytes = GEO::g > 0 ? GEO::GROUPS * GEO::XSTRIDE * 4 : 0;
-  const int ss_bytes = ((GEO::FPW * fp.num_sub * 2) + 15) & ~15;
+  const int ss_bytes = (((GEO::FPW * fp.num_sub * 2) + 15) & ~15) + (PN::kActive ? 2 * GEO::FPW * 48 : 0);
   auto layout = [&](int smem_rows) {
     const int dec_bytes = smem_rows * 32 * 4;
     fp.smem_rows = smem_rows;
     fp.dec_off = 0;
     fp.x_off = dec_bytes;
     fp.ss_off = dec_bytes + x_bytes;
+    fp.stg_off = fp.ss_off + (((GEO::FPW * fp.num_sub * 2) + 15) & ~15);  // staging ring after the start states
     fp.smem_per_warp = (dec_bytes + x_bytes + ss_bytes + 15) & ~15;
   };
   // Tensor-memory survivor store: W warps per CTA (W/4 per TMEM lane quarter)
@@ -1538,6 +1703,36 @@ bool try_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
   Plan pl;
   if (!plan<C, R>(p, &pl)) return false;
   if (err) *err = launch_variant<C, R>(p, stream);
+  return true;
+}
+
+/// Fused-depuncture launch: p.llr is the PUNCTURED stream (pattern PN, stage
+/// 0 at byte 0); the fast kernel decodes the interior frames [*mi0, *mi1)
+/// it can take, the caller decodes the rest from a dense copy. Returns false
+/// (nothing launched) when the plan needs more than TMEM + shared memory.
+template <class C, int R, class PN>
+bool try_punct_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
+                       std::int64_t* mi1) {
+  using GEO = Geo<C, R>;
+  if (!C::matches(p.k, p.b, p.polys)) return false;
+  if (p.f % PN::P || p.v1 % PN::P || p.v2 % PN::P) return false;
+  Plan pl;
+  if (!plan<C, R, PN>(p, &pl) || !pl.tm || pl.gl) return false;
+  *mi0 = pl.fp.mi0;
+  *mi1 = pl.fp.mi1;
+  if (!stream && !err) return true;  // probe
+  const FastParams& fp = pl.fp;
+  auto kern = fast_kernel<C, R, true, false, PN>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(pl.smem));
+  if (e == cudaSuccess) {
+    const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
+    std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
+    blocks = std::min<std::int64_t>(blocks, static_cast<std::int64_t>(sm_count()));
+    kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fp);
+    note_launch();
+    e = cudaGetLastError();
+  }
+  *err = e;
   return true;
 }
 

@@ -91,6 +91,12 @@ constexpr int kPfSlackStages = 12;
 /// code/config is outside its envelope (caller then uses the generic one).
 bool fast_path_supported(const DecodeLaunch& p);
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream);
+/// Fused depuncture (pattern 23: "11;10", 34: "110;101"; B = 2 codes with a
+/// fused instantiation): p.llr is the punctured stream; launches the fast
+/// kernel over the interior frames [*mi0, *mi1) it takes (stream == nullptr
+/// and err == nullptr: plan only). False: not supported for this code/config.
+bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err,
+                          std::int64_t* mi0, std::int64_t* mi1);
 /// Exact segment-parallel decode of one long frame (serial_decode, f >= N;
 /// max-plus transfer matrices, vd_serial.cu). S <= 64, B in {2, 3}, int8.
 bool serial_parallel_supported(const DecodeLaunch& p);

@@ -248,3 +248,44 @@ def test_drop_in_depuncture_f64_matches_reference(name):
         got = np.zeros(n_stages.value * b, np.float64)
         check(lib().vd_depuncture_f64(C.byref(pc), d.ctypes.data, n_p, got.ctypes.data))
         assert np.array_equal(got, out[:n_stages.value * b]), (name, n_p)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("pattern,cfg", [("r23", (256, 20, 20)), ("r23", (128, 16, 42)), ("r34", (255, 21, 21)),
+                                         ("r34", (240, 24, 48))])
+def test_fused_depuncture_device_decode(pattern, cfg, monkeypatch):
+    """Depuncture fused into the fast kernel's LLR staging (vd_fast.cuh
+    Punct: the kernel gathers the punctured stream into its shared-memory LLR
+    ring, re-inserting the zeros) == the oracle's framed_decode of the
+    depunctured block, and == the separate-pass path (VITDEC_PUNCT_FUSED=0);
+    edge frames come from dense copies of their windows."""
+    import ctypes as C
+
+    import torch
+
+    k, b, polys = K7
+    rows = _rows(pattern)
+    t = vd.build_trellis(vd.CodeSpec(k, b, polys))
+    p = vd.PuncturePattern.parse(rows)
+    fc = vd.FrameConfig(*cfg)
+    for n_stages in (cfg[0] * 40 + 7, 200_001, 1 << 20):
+        punct, sent = _punctured_case(k, b, polys, rows, n_stages, seed=n_stages + cfg[0])
+        full, n = oracle.depuncture_i8(rows, punct)
+        exp, st, _ = oracle.port().framed_decode(k, b, polys, full, n, fc.f, fc.v1, fc.v2)
+        dev_in = torch.from_numpy(punct.copy()).cuda()
+        res = {}
+        for fused in ("1", "0"):
+            monkeypatch.setenv("VITDEC_PUNCT_FUSED", fused)
+            scratch = torch.empty(n * b, dtype=torch.int8, device="cuda")
+            out = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")  # stale bits must be cleared
+            s = vd.api.VdStats()
+            c, pc = fc.to_c(), p.to_c()
+            vd.api.check(vd.lib().vd_decode_punctured_i8_device(t.handle, C.byref(c), C.byref(pc), dev_in.data_ptr(),
+                                                                punct.size, scratch.data_ptr(), out.data_ptr(),
+                                                                C.byref(s), -1, None))
+            torch.cuda.synchronize()
+            res[fused] = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
+            assert (s.frames, s.stages, s.tracebacks) == st
+        bad = np.flatnonzero(res["1"] != exp)
+        assert bad.size == 0, (pattern, cfg, n_stages, bad[:10], bad.size)
+        assert np.array_equal(res["0"], exp)

@@ -90,7 +90,15 @@ def main():
         punct = torch.from_numpy(punct_h).cuda()
         scratch = torch.empty(n * 2, dtype=torch.int8, device="cuda")
         dep_s = timed(lambda: depuncture_i8_device(p, punct, punct_h.size, scratch, -1, s))
+        import os
+
+        os.environ["VITDEC_PUNCT_FUSED"] = "0"  # A/B: separate depuncture pass + decode
         dec_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
+        sep_out = out.clone()
+        os.environ["VITDEC_PUNCT_FUSED"] = "1"  # depuncture fused into the fast kernel's LLR staging
+        fused_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
+        fused_same = bool(torch.equal(out[: n // 32], sep_out[: n // 32]))
+        os.environ.pop("VITDEC_PUNCT_FUSED")
         # correctness: the depunctured block equals the oracle's (sampled), decode equals the block decode
         want, _ = oracle.depuncture_i8(rows, punct_h[: min(punct_h.size, 1 << 24) // p.kept_per_period()
                                                      * p.kept_per_period()])
@@ -109,7 +117,8 @@ def main():
                            "frac": dep_bytes / dep_s / 1e9 / peaks["hbm_gbs"], "bytes": dep_bytes,
                            "matches_oracle": ok_dep},
             "device_gbps": {"unpunctured_decode": n / base_s / 1e9, "depuncture_plus_decode": n / dec_s / 1e9,
-                            "depuncture_share": dep_s / dec_s},
+                            "depuncture_share": dep_s / dec_s, "fused_depuncture_decode": n / fused_s / 1e9,
+                            "fused_vs_separate": dec_s / fused_s, "fused_matches_separate": fused_same},
             "e2e_gbps": {"unpunctured": ne / e2e_full / 1e9, "punctured": ne / e2e_p / 1e9,
                          "h2d_bytes_punctured": int(pe.size), "h2d_bytes_unpunctured": ne * 2},
         }))

@@ -16,17 +16,22 @@ FMAH = {"VIADD.16x2", "IMAD", "IMAD.IADD", "IMAD.MOV.U32", "IMAD.X", "IMAD.SHL.U
 
 def main():
     obj = sys.argv[1] if len(sys.argv) > 1 else "paper_2011_09337_b200/build/vd_fast_k7.o"
-    pat = sys.argv[2] if len(sys.argv) > 2 else "CodeBILi7ELi2ELj121ELj91ELj0EEELi16ELb1ELb0E"
+    pat = sys.argv[2] if len(sys.argv) > 2 else "CodeBILi7ELi2ELj121ELj91ELj0EEELi16ELb1ELb0ENS0_7NoPunct"
     txt = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", txt)
     f = next(x for x in funcs if pat in x.split("\n")[0])
     ins = [(int(a, 16), t.strip()) for a, t in re.findall(r"/\*([0-9a-f]{4,})\*/\s+([^;]*);", f)]
     sttm = [i for i, (_, t) in enumerate(ins) if "STTM.x4" in t]
-    j = sttm[-1]
-    while "BRA" not in ins[j][1]:
-        j += 1
-    tgt = int(re.search(r"0x([0-9a-f]+)", ins[j][1].split("BRA")[1]).group(1), 16)
-    lo = next(i for i, (a, _) in enumerate(ins) if a == tgt)
+    addr_idx = {a: i for i, (a, _) in enumerate(ins)}
+    best = None  # innermost backward branch whose loop holds both STTM.x4 blocks
+    for j, (a, t) in enumerate(ins):
+        m = re.search(r"BRA\S*\s+(?:\S+,\s*)?0x([0-9a-f]+)", t)
+        if not m:
+            continue
+        lo = addr_idx.get(int(m.group(1), 16))
+        if lo is not None and lo <= sttm[0] and j >= sttm[-1] and (best is None or j - lo < best[1] - best[0]):
+            best = (lo, j)
+    lo, j = best
     body = [t for _, t in ins[lo:j + 1]]
     ops = collections.Counter(re.sub(r"^@!?U?P\w+\s+", "", t).split()[0] for t in body)
     blocks = len(sttm)
