@@ -310,12 +310,10 @@ struct FastParams {
   std::int64_t head_pitch;  // stages per block in llr_head (batched: v1 + head window)
   int tm_alloc;  // TMEM columns allocated per CTA (power of two)
   std::int64_t safe_stage;  // window start of an interior frame (loads of empty frame slots)
-  // IMAD multiplier 2 read from the parameter bank: ptxas cannot constant-fold
-  // it, so the decision arithmetic written as mad_u32 stays on the FMA pipe
-  // instead of becoming ALU-pipe LEA / IADD3.
-  // (field order matters: two and m1 adjacent made ptxas load them as one
-  // 64-bit uniform pair and copy them into registers in every block)
-  std::uint32_t two, pad0, m1;
+  // -1 read from the parameter bank: ptxas cannot constant-fold it, so the
+  // table negations written as mad_u32 stay IMADs on the FMA pipe instead of
+  // becoming ALU-pipe IADD3s.
+  std::uint32_t m1;
 };
 
 // Opaque copy: keeps a per-lane constant in a register instead of letting the
@@ -351,10 +349,6 @@ __device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t 
 // Compile-time tuning knobs (the defaults are the measured-best settings;
 // every rejected alternative is logged in profiles/r01_ab_notes.md /
 // profiles/r02_ab_notes.md and was removed from the source).
-#ifndef VD_FMA_PAIRS
-#define VD_FMA_PAIRS 6      // butterflies per stage with FMA-pipe decision words (rest: ALU form)
-#endif
-constexpr int kFmaPairs = VD_FMA_PAIRS;
 #ifndef VD_NEG_FMA
 #define VD_NEG_FMA 1        // negated branch tables as IMAD (param-bank -1) on the FMA pipe (C5 +0.5 %, C4 +0.9 %)
 #endif
@@ -386,15 +380,6 @@ constexpr int max_warps() {
   return VD_MAX_WARPS ? VD_MAX_WARPS : (C::kK >= 9 ? 16 : 12);
 }
 
-// (a & m) | (b & ~m) as one LOP3 that the compiler cannot re-associate into a
-// serial chain (keeps the decision-compaction tree 3 deep).
-template <std::uint32_t MASK>
-__device__ __forceinline__ std::uint32_t bitsel(std::uint32_t a, std::uint32_t b) {
-  std::uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0xE4;" : "=r"(r) : "r"(a), "r"(b), "n"(MASK));  // 0xE4: c ? a : b
-  return r;
-}
-
 // (a & m) | (b & ~m) as one LOP3 (m a compile-time constant after unrolling)
 __device__ __forceinline__ std::uint32_t bitsel_m(std::uint32_t a, std::uint32_t b, std::uint32_t m) {
   std::uint32_t r;
@@ -402,24 +387,33 @@ __device__ __forceinline__ std::uint32_t bitsel_m(std::uint32_t a, std::uint32_t
   return r;
 }
 
-// 32 decisions (16 registers x 2 frames) -> one word, bit (rho + 16 * half).
-// The source words carry !decision in bits 15 / 31; the last merge inverts.
-__device__ __forceinline__ std::uint32_t bitsel_not(std::uint32_t a, std::uint32_t b) {
-  std::uint32_t r;
-  asm("lop3.b32 %0, %1, %2, %3, 0x1B;" : "=r"(r) : "r"(a), "r"(b), "n"(0x0f0f0f0fu));  // ~(c ? a : b)
-  return r;
+template <std::uint32_t MUL>
+__device__ __forceinline__ std::uint32_t mad_imm(std::uint32_t a, std::uint32_t c) {
+  std::uint32_t d;
+  asm("mad.lo.u32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "n"(MUL), "r"(c));
+  return d;
 }
-__device__ __forceinline__ std::uint32_t compact16(const std::uint32_t* w) {
+// 32 decisions (16 registers x 2 frames) -> one word, bit (rho + 16 * half).
+// The source words carry !decision in bits 15 / 31; m1 = -1 (parameter bank).
+__device__ __forceinline__ std::uint32_t compact16(const std::uint32_t* w, std::uint32_t m1) {
   std::uint32_t y[8];
 #pragma unroll
   for (int q = 0; q < 8; ++q) y[q] = prmt(w[q], w[q + 8], 0xFBD9u);
-  const std::uint32_t a = bitsel<0x01010101u>(y[0], y[1]);
-  const std::uint32_t b = bitsel<0x04040404u>(y[2], y[3]);
-  const std::uint32_t c = bitsel<0x10101010u>(y[4], y[5]);
-  const std::uint32_t d = bitsel<0x40404040u>(y[6], y[7]);
-  const std::uint32_t ab = bitsel<0x03030303u>(a, b);
-  const std::uint32_t cd = bitsel<0x30303030u>(c, d);
-  return bitsel_not(ab, cd);
+  // Merge on the FMA pipe: y[q] = 255 * N_q with N_q the 4 !decision bits
+  // of PRMT q at bit 8j of byte j, and 255 * 0x01010101 = -1 (mod 2^32), so
+  // sum_q y[q] * (0x01010101 << q) = -sum_q N_q << q = -Xn, where Xn holds
+  // !decision (reg, half) at bit reg + 16 * half; -1 - Xn = ~Xn is the
+  // decision word. Eight IMADs instead of a 7-LOP3 merge tree: the ALU pipe
+  // (VIADDMNMX, IADD3, PRMT) was the binding pipe (C5 +4 %, C3 +4 %,
+  // profiles/r02_ab_notes.md).
+  std::uint32_t acc = mad_imm<0x01010101u>(y[0], m1);
+  acc = mad_imm<0x02020202u>(y[1], acc);
+  acc = mad_imm<0x04040404u>(y[2], acc);
+  acc = mad_imm<0x08080808u>(y[3], acc);
+  acc = mad_imm<0x10101010u>(y[4], acc);
+  acc = mad_imm<0x20202020u>(y[5], acc);
+  acc = mad_imm<0x40404040u>(y[6], acc);
+  return mad_imm<0x80808080u>(y[7], acc);
 }
 
 template <class GEO>
@@ -433,7 +427,6 @@ struct FrameState {
   std::uint32_t fw[GEO::WPB];
   std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : 3];
   std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
-  std::uint32_t two_p;                // 2 from the parameter bank (not constant-folded by ptxas)
   std::uint32_t m1_p;                 // -1 from the parameter bank
   std::uint32_t corr;                 // pending renormalisation (BASE - ref per half)
 };
@@ -585,7 +578,6 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
     const int t = blk * LB + k;
     std::uint32_t* w = st.wv[k & 1];
     // ---- add-compare-select, in place: E/O registers differ in bit k -------
-    int pair = 0;
 #pragma unroll
     for (int e = 0; e < R; ++e) {
       if ((e >> k) & 1) continue;
@@ -601,26 +593,18 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       // per half keeps each half in [0, 0xFFFE], so no carry crosses halves.
       // (MODE 3: warm-up stages t < v1 keep no decisions, decoder.cpp:229-235
       // never reads them.)
-      if constexpr (MODE == 3) {
-      } else if (pair < kFmaPairs) {
-        // FMA-pipe form: (sE - sO) + (PT[x] - PT[x ^ XM] + 0x7FFF) =
-        // d' + 2 PT[x] with d' = sE - sO + 0x7FFF - OFFB per half (one IADD3),
-        // then two IMADs with a multiplier ptxas cannot see
-        const std::uint32_t dp = sE - sO + (0x7fff7fffu - OFFB);
-        w[e] = mad_u32(PT[k][x], st.two_p, dp);
-        w[od] = mad_u32(PT[k][x ^ XM], st.two_p, dp);
-      } else {
-        // ALU-pipe form: new - s2 (>= 0, 0 iff the second won) + 0x7FFF, 1 IADD3 each
+      if constexpr (MODE != 3) {
+        // new - s2 (>= 0, 0 iff the second won) + 0x7FFF: one IADD3 per two
+        // decisions (measured faster than an FMA-pipe form for some of them)
         w[e] = nL - s2L + 0x7fff7fffu;
         w[od] = nH - s2H + 0x7fff7fffu;
       }
       st.sig[e] = nL;
       st.sig[od] = nH;
-      ++pair;
     }
     // ---- previous stage's decisions -> survivor store (overlaps this ACS) --
     if constexpr (MODE == 3) continue;
-    const std::uint32_t word = compact16(st.wv[(k + 1) & 1]);
+    const std::uint32_t word = compact16(st.wv[(k + 1) & 1], st.m1_p);
     if constexpr (MODE == 0) {
       store_dec<TM, GL>(bc, tprev, word);
       tprev = t;
@@ -832,7 +816,6 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
 #pragma unroll
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);
   }
-  st.two_p = fp.two;
   st.m1_p = fp.m1;
   st.corr = 0u;
 #pragma unroll
@@ -1077,7 +1060,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     }
   }
   // decisions of the last processed stage
-  store_dec<TM, GL>(bc, tprev, compact16(st.wv[(nblk * LB - 1) & 1]));
+  store_dec<TM, GL>(bc, tprev, compact16(st.wv[(nblk * LB - 1) & 1], st.m1_p));
   if constexpr (TM) asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
   __syncwarp();
 
@@ -1466,7 +1449,6 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   fp.llr_head = p.llr_head;
   fp.head_pitch = p.head_pitch;
   fp.p = p;
-  fp.two = 2u;
   fp.m1 = 0xffffffffu;
   fp.L = p.f + p.v1 + p.v2;
   fp.nblk = (fp.L + GEO::LB - 1) / GEO::LB;
