@@ -1367,13 +1367,16 @@ vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg*
   DeviceGuard guard(dev);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const std::int64_t nf = num_frames(cfg, n);
-  // Fused depuncture (vd_fast.cuh Punct): the fast kernel stages the
-  // punctured stream straight into its shared-memory LLR ring; the few edge
-  // frames it does not take are decoded from dense copies of their windows.
-  // VITDEC_PUNCT_FUSED=0 selects the separate depuncture pass (A/B).
+  // Fused depuncture (vd_fast.cuh Punct, VITDEC_PUNCT_FUSED=1): the fast
+  // kernel stages the punctured stream straight into its shared-memory LLR
+  // ring; the few edge frames it does not take are decoded from dense copies
+  // of their windows. Off by default: measured against the separate
+  // HBM-streaming depuncture pass on one B200 (2^30 stages, f=240/24/24) it
+  // ran at 0.99x (r2/3) and 0.54x (r3/4) of pass + decode
+  // (profiles/r02_puncture_bench.jsonl, profiles/r02_ab_notes.md).
   const int pid = punct_pattern_id(pp);
   const char* env_fused = std::getenv("VITDEC_PUNCT_FUSED");
-  const bool want_fused = pid != 0 && (!env_fused || std::atoi(env_fused) != 0) &&
+  const bool want_fused = pid != 0 && env_fused && std::atoi(env_fused) != 0 &&
                           (reinterpret_cast<std::uintptr_t>(punctured_dev) & 3u) == 0 && cfg->f0 == 0;
   if (want_fused && check_gpu_envelope(code) == VD_OK) {
     vd::DecodeLaunch p;

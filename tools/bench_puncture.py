@@ -90,19 +90,21 @@ def main():
         punct = torch.from_numpy(punct_h).cuda()
         scratch = torch.empty(n * 2, dtype=torch.int8, device="cuda")
         dep_s = timed(lambda: depuncture_i8_device(p, punct, punct_h.size, scratch, -1, s))
-        import os
-
-        os.environ["VITDEC_PUNCT_FUSED"] = "0"  # A/B: separate depuncture pass + decode
-        dec_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
-        sep_out = out.clone()
-        os.environ["VITDEC_PUNCT_FUSED"] = "1"  # depuncture fused into the fast kernel's LLR staging
-        fused_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
-        fused_same = bool(torch.equal(out[: n // 32], sep_out[: n // 32]))
-        os.environ.pop("VITDEC_PUNCT_FUSED")
-        # correctness: the depunctured block equals the oracle's (sampled), decode equals the block decode
+        # correctness: the depunctured block (the separate pass's output, read
+        # before the fused run rewrites the scratch with its edge windows) equals
+        # the oracle's on a sampled prefix
         want, _ = oracle.depuncture_i8(rows, punct_h[: min(punct_h.size, 1 << 24) // p.kept_per_period()
                                                      * p.kept_per_period()])
         ok_dep = bool(np.array_equal(scratch[: want.size].cpu().numpy(), want))
+        import os
+
+        os.environ["VITDEC_PUNCT_FUSED"] = "0"  # A/B: separate depuncture pass + decode (default)
+        dec_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
+        sep_out = out.clone()
+        os.environ["VITDEC_PUNCT_FUSED"] = "1"  # depuncture fused into the fast kernel's LLR staging (opt-in)
+        fused_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
+        fused_same = bool(torch.equal(out[: n // 32], sep_out[: n // 32]))
+        os.environ.pop("VITDEC_PUNCT_FUSED")
         # e2e host-buffer punctured call on the first ne stages
         pe = oracle.puncture_i8(rows, full_h[: ne * 2], ne)
         host_p = torch.from_numpy(pe).pin_memory()
