@@ -76,6 +76,8 @@ def parse():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-weak", action="store_true", help="skip the secondary weak-scaling line (N > 1)")
     ap.add_argument("--frame", default="", help="f,v1,v2[,f0] frame configuration override (default 256,20,20)")
+    ap.add_argument("--polys", default="", help="octal generator polynomials overriding the workload's code "
+                    "(same K and B; e.g. 165,117: a code served by a run-time kernel instantiation)")
     a = ap.parse_args()
     if a.frame:
         global F, V1, V2, F0
@@ -83,6 +85,14 @@ def parse():
         F, V1, V2 = vals[:3]
         F0 = vals[3] if len(vals) > 3 else 0
     a.code, default_n, a.workload_desc = WORKLOADS[a.workload]
+    if a.polys:
+        k, b, _ = a.code
+        polys = [int(x, 8) for x in a.polys.split(",")]
+        if len(polys) != b or any(p >> k for p in polys):
+            raise SystemExit(f"--polys needs {b} polynomials of at most K={k} bits")
+        a.code = (k, b, polys)
+        a.workload_desc += f", code overridden: ({','.join(oct(p)[2:] for p in polys)})"
+
     if a.stages <= 0:
         a.stages = default_n
     return a

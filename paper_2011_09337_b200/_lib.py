@@ -59,6 +59,7 @@ SIGNATURES = {
     "vd_code_b": (I32, [P]),
     "vd_code_tables": (I32, [P, P, P, P, P, P]),
     "vd_code_fast_path": (I32, [P]),
+    "vd_code_jit_check": (I32, [P]),
     "vd_frame_cfg_validate": (I32, [C.POINTER(VdFrameCfg), I32]),
     "vd_frame_stats": (I32, [C.POINTER(VdFrameCfg), I64, C.POINTER(VdStats)]),
     "vd_partition_frames": (I32, [C.POINTER(VdFrameCfg), I64, I32, P]),

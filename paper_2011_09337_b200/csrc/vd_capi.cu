@@ -58,7 +58,9 @@ vd_status fail(vd_status st, const std::string& msg) {
 
 vd_status cuda_fail(cudaError_t e, const char* what) {
   cudaGetLastError();  // clear sticky-free errors
-  return fail(VD_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  std::string msg = std::string(what) + ": " + cudaGetErrorString(e);
+  if (e == cudaErrorInvalidSource && !vd::jit::last_log().empty()) msg += " (" + vd::jit::last_log() + ")";
+  return fail(VD_ECUDA, msg);
 }
 
 #define VD_CUDA(call, what)                         \
@@ -1154,6 +1156,14 @@ int32_t vd_code_fast_path(const vd_code* code) {
   for (int i = 0; i < code->b && i < 8; ++i) p.polys[i] = code->polys[i];
   p.complement_paired = code->complement_paired;
   return vd::fast_path_supported(p) ? 1 : 0;
+}
+
+vd_status vd_code_jit_check(const vd_code* code) {
+  if (!code) return fail(VD_EINVAL, "null code");
+  if (!vd::fast_envelope_code(code->k, code->b, code->polys.data()))
+    return fail(VD_EUNSUPPORTED, "code outside the fast kernel's envelope (complement-paired, 5 <= K <= 9, B in {2, 3})");
+  if (!vd::jit::compile_check(code->k, code->b, code->polys.data())) return fail(VD_ECUDA, vd::jit::last_log());
+  return VD_OK;
 }
 
 vd_status vd_frame_cfg_validate(const vd_frame_cfg* cfg, int32_t pattern_period) {

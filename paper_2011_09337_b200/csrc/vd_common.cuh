@@ -6,7 +6,7 @@
 // same states on the GPU as on the CPU.
 #pragma once
 
-#include <cstdint>
+#include "vd_std.h"
 
 #ifdef __CUDACC__
 #define VD_HD __host__ __device__ __forceinline__

@@ -1,6 +1,7 @@
 // Fast-kernel dispatch (the kernels and their planning: vd_fast.cuh; the
-// per-code instantiations: vd_fast_k*.cu) and the zero-padded block-head
-// gather used by the batched decode.
+// per-code instantiations: vd_fast_k*.cu; other codes: run-time
+// instantiations, vd_jit.cu) and the zero-padded block-head gather used by
+// the batched decode.
 #include "vd_fast.cuh"
 
 namespace vd {
@@ -12,6 +13,49 @@ bool try_group_k9(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, 
 bool try_group_k568(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe);
 bool try_punct_k7(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
                   std::int64_t* mi1);
+
+// ---- run-time instantiations (vd_jit.cu) for other complement-paired codes --
+// plan() uses only K and B of its code, so one placeholder code per (K, B)
+// class plans every code of the class; the kernel comes from the JIT.
+template <int K, int B>
+using PlanCode = CodeB<K, B, (1u << (K - 1)) | 1u, (1u << (K - 1)) | 1u, B == 3 ? ((1u << (K - 1)) | 1u) : 0u>;
+
+struct JitSel {
+  const DecodeLaunch* p;
+  const void* operator()(bool tm, bool gl, cudaError_t* e) const {
+    return jit::fast_kernel(p->k, p->b, p->polys, tm, gl, e);
+  }
+};
+
+template <int K, int B>
+bool try_jit_kb(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe) {
+  Plan pl;
+  if (!plan<PlanCode<K, B>, 16>(p, &pl)) return false;
+  if (!probe) *err = launch_variant<PlanCode<K, B>, 16>(p, stream, JitSel{&p});
+  return true;
+}
+
+// The fast kernel's envelope: 5 <= K <= 9 (16 states per lane; int16 metric
+// range), B in {2, 3}, every polynomial tapping the newest
+// and the oldest register bit (both butterfly edges are complement pairs).
+bool jit_code(const DecodeLaunch& p) { return jit::enabled() && fast_envelope_code(p.k, p.b, p.polys); }
+
+bool try_jit(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe) {
+  if (!jit_code(p)) return false;
+  switch (p.k * 10 + p.b) {
+    case 52: return try_jit_kb<5, 2>(p, stream, err, probe);
+    case 53: return try_jit_kb<5, 3>(p, stream, err, probe);
+    case 62: return try_jit_kb<6, 2>(p, stream, err, probe);
+    case 63: return try_jit_kb<6, 3>(p, stream, err, probe);
+    case 72: return try_jit_kb<7, 2>(p, stream, err, probe);
+    case 73: return try_jit_kb<7, 3>(p, stream, err, probe);
+    case 82: return try_jit_kb<8, 2>(p, stream, err, probe);
+    case 83: return try_jit_kb<8, 3>(p, stream, err, probe);
+    case 92: return try_jit_kb<9, 2>(p, stream, err, probe);
+    case 93: return try_jit_kb<9, 3>(p, stream, err, probe);
+    default: return false;
+  }
+}
 
 __global__ void head_gather_kernel(const std::int8_t* __restrict__ llr, const std::int64_t* __restrict__ blk_stage,
                                    int nblocks, int b, int v1, std::int64_t pitch, std::int64_t copy,
@@ -43,12 +87,20 @@ cudaError_t launch_head_gather(const std::int8_t* llr, const std::int64_t* blk_s
   return cudaGetLastError();
 }
 
+bool fast_envelope_code(int k, int b, const std::uint32_t* polys) {
+  if (k < 5 || k > 9 || (b != 2 && b != 3)) return false;
+  for (int i = 0; i < b; ++i) {
+    if (!(polys[i] & 1u) || !((polys[i] >> (k - 1)) & 1u)) return false;
+  }
+  return true;
+}
+
 bool fast_path_supported(const DecodeLaunch& p) {
   using namespace fast;
   if (p.b != 2 && p.b != 3) return false;
   cudaError_t unused = cudaSuccess;
   return try_group_k7(p, nullptr, &unused, true) || try_group_k9(p, nullptr, &unused, true) ||
-         try_group_k568(p, nullptr, &unused, true);
+         try_group_k568(p, nullptr, &unused, true) || try_jit(p, nullptr, &unused, true);
 }
 
 bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err,
@@ -62,6 +114,7 @@ cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream) {
   if (try_group_k7(p, stream, &err, false)) return err;
   if (try_group_k9(p, stream, &err, false)) return err;
   if (try_group_k568(p, stream, &err, false)) return err;
+  if (try_jit(p, stream, &err, false)) return err;
   return cudaErrorNotSupported;
 }
 

@@ -5,71 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <string>
+
+#include "vd_launch.h"
 
 namespace vd {
-
-/// Everything a decode launch needs. Pointers are device pointers.
-struct DecodeLaunch {
-  int k = 0, b = 0, s = 0;
-  int f = 0, v1 = 0, v2 = 0, f0 = 0, start = 0;
-  std::uint64_t seed = 0;
-  std::int64_t n = 0;                     // stream length in stages
-  std::int64_t frame_begin = 0, frame_end = 0;
-  const void* llr = nullptr;              // LLRs of stage llr_stage0
-  std::int64_t llr_stage0 = 0;
-  std::uint32_t* out = nullptr;           // packed bits of stage out_stage0 (word aligned)
-  std::int64_t out_stage0 = 0;
-  void* sigma = nullptr;                  // optional final metrics [frames][S]
-  const std::uint32_t* in_out = nullptr;  // device copy of Trellis::in_out_ [S*2]
-  std::uint32_t polys[8] = {};
-  bool complement_paired = false;
-  // Batched mode (nblocks > 0): the stream is the concatenation of nblocks
-  // independent blocks (reference run_ber_sweep decodes every block with its
-  // own framed_decode call, berlab.cpp:63-88). Block j spans stages
-  // [blk_stage[j], blk_stage[j+1]) and global frames [blk_frame[j],
-  // blk_frame[j+1]); its frames are clipped at the block ends and their
-  // random-start salt uses the block-local frame index. Frame indices in
-  // [frame_begin, frame_end) are global; n is the total stage count.
-  int nblocks = 0;
-  const std::int64_t* blk_stage = nullptr;  // device [nblocks + 1]
-  const std::int64_t* blk_frame = nullptr;  // device [nblocks + 1]
-  const std::int32_t* blk_ilo = nullptr;    // device [nblocks]: fast-kernel frames are local [ilo, ihi)
-  const std::int32_t* blk_ihi = nullptr;
-  // Generic kernels only: process frame_list[frame_begin .. frame_end) (global
-  // frame ids) instead of the index range itself.
-  const std::int64_t* frame_list = nullptr;
-  std::int64_t safe_stage = 0;  // batched fast launch: window start of some interior frame
-  // Fast kernel only: frames whose window is clipped by their block start
-  // (m*f < v1) read a zero-padded copy of the block head instead:
-  // llr_head[(blk * head_pitch + (t + v1)) * b] = stage t of block blk.
-  const std::int8_t* llr_head = nullptr;
-  std::int64_t head_pitch = 0;
-};
-
-/// A global frame id resolved to its block: block-local frame index, block
-/// length and the block's first stage in the concatenated stream.
-struct FrameRef {
-  std::int64_t m, n, base;
-  int blk;
-};
-
-#ifdef __CUDACC__
-__device__ __forceinline__ FrameRef resolve_frame(const DecodeLaunch& p, std::int64_t idx) {
-  const std::int64_t g = p.frame_list ? __ldg(p.frame_list + idx) : idx;
-  if (p.nblocks == 0) return FrameRef{g, p.n, 0, 0};
-  int lo = 0, hi = p.nblocks;  // blk_frame[lo] <= g < blk_frame[hi]
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (__ldg(p.blk_frame + mid) <= g) {
-      lo = mid;
-    } else {
-      hi = mid;
-    }
-  }
-  const std::int64_t b0 = __ldg(p.blk_stage + lo);
-  return FrameRef{g - __ldg(p.blk_frame + lo), __ldg(p.blk_stage + lo + 1) - b0, b0, lo};
-}
-#endif
 
 /// Generic sm_100a kernels (any K in [2, 16], B in [2, 8]); int8 LLRs with
 /// int32 metrics or double LLRs with double metrics. K <= kMaxGenericK: warp
@@ -97,6 +37,19 @@ cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream);
 /// and err == nullptr: plan only). False: not supported for this code/config.
 bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err,
                           std::int64_t* mi0, std::int64_t* mi1);
+namespace jit {
+/// Run-time (NVRTC) instantiation of the fast kernel for a code outside the
+/// precompiled list (vd_jit.cu); nullptr + *err (cudaErrorInvalidSource:
+/// compile failure, see last_log()) on failure. VITDEC_JIT=0 disables it.
+bool enabled();
+const void* fast_kernel(int k, int b, const std::uint32_t* polys, bool tm, bool gl, cudaError_t* err);
+const std::string& last_log();
+/// Compile only (no GPU needed): false + last_log() on failure.
+bool compile_check(int k, int b, const std::uint32_t* polys);
+}  // namespace jit
+/// Complement-paired code inside the fast kernel's envelope (vd_fast.cu).
+bool fast_envelope_code(int k, int b, const std::uint32_t* polys);
+
 /// Exact segment-parallel decode of one long frame (serial_decode, f >= N;
 /// max-plus transfer matrices, vd_serial.cu). S <= 64, B in {2, 3}, int8.
 bool serial_parallel_supported(const DecodeLaunch& p);

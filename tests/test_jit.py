@@ -1,0 +1,83 @@
+"""Run-time (NVRTC) instantiations of the fast kernel for codes outside the
+precompiled list (csrc/vd_jit.cu).
+
+The reference's ACS is code-generic through the trellis tables
+(proj/src/decoder.cpp:53-76, trellis.cpp:57-100); the fast kernel bakes the
+polynomials into compile-time table selections, so every complement-paired
+code with 5 <= K <= 9 and B in {2, 3} gets its own instantiation compiled on
+first use. CPU tests: the envelope and the NVRTC compile of the embedded
+sources (no GPU needed). GPU tests: bit-exact parity with the oracle and
+identical results with the JIT disabled (generic kernel).
+"""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2011_09337_b200 as vd
+
+# complement-paired codes that are NOT among the precompiled instantiations
+JIT_CODES = [
+    (7, 2, [0o165, 0o117]),
+    (7, 3, [0o171, 0o133, 0o145]),
+    (5, 3, [0o25, 0o33, 0o37]),
+    (6, 2, [0o65, 0o57]),
+    (8, 3, [0o225, 0o331, 0o367]),
+    (9, 2, [0o657, 0o435]),
+]
+
+
+def trellis(spec):
+    k, b, polys = spec
+    return vd.build_trellis(vd.CodeSpec(k, b, list(polys)))
+
+
+def test_jit_envelope(monkeypatch):
+    lib = vd.lib()
+    for spec in JIT_CODES:
+        assert trellis(spec).fast_path(), spec
+    # not complement-paired (0170 misses the oldest tap) -> generic kernel
+    t = trellis((7, 2, [0o170, 0o133]))
+    assert not t.fast_path()
+    assert lib.vd_code_jit_check(t.handle) == vd.api.VD_EUNSUPPORTED
+    # K outside 5..9
+    assert not trellis((4, 2, [0o17, 0o13])).fast_path()
+    assert not trellis((10, 2, [0o1157, 0o1753])).fast_path()
+    monkeypatch.setenv("VITDEC_JIT", "0")
+    assert not trellis(JIT_CODES[0]).fast_path()
+    assert trellis((7, 2, [0o171, 0o133])).fast_path()  # precompiled: unaffected
+
+
+def test_jit_compiles_embedded_sources():
+    """NVRTC compiles the sources embedded in the library for sm_100a (what a
+    GPU box does on first use of a new code)."""
+    t = trellis(JIT_CODES[0])
+    st = vd.lib().vd_code_jit_check(t.handle)
+    assert st == 0, vd.lib().vd_last_error()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", JIT_CODES, ids=lambda s: f"K{s[0]}B{s[1]}")
+def test_jit_fast_path_vs_oracle(spec, monkeypatch, tmp_path):
+    monkeypatch.setenv("VITDEC_JIT_CACHE", str(tmp_path))  # compile in this test, not from a cache
+    k, b, polys = spec
+    port = oracle.port()
+    t = trellis(spec)
+    assert t.fast_path()
+    rng = np.random.default_rng(7000 + k * 10 + b)
+    # TMEM + smem survivor store; subframe tracebacks; long frames (global spill tier)
+    cfgs = [vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 45, 32), vd.FrameConfig(1024, 42, 42)]
+    for i, cfg in enumerate(cfgs):
+        n = int(rng.integers(150_000, 220_000))
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(1, 4)), 11 + i)
+        q = oracle.quantize(rx, [32.0, 4.0][i % 2])
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0)
+        packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+        got = vd.unpack_bits(packed, n)
+        bad = np.flatnonzero(got != exp)
+        assert bad.size == 0, (spec, cfg, n, bad[:10], bad.size)
+        assert (stats.frames, stats.stages, stats.tracebacks) == st
+        if i == 0:
+            monkeypatch.setenv("VITDEC_JIT", "0")  # generic kernel: same bits
+            packed0, _ = vd.framed_decode_stream(q, n, t, cfg)
+            assert np.array_equal(vd.unpack_bits(packed0, n), exp)
+            monkeypatch.delenv("VITDEC_JIT")
