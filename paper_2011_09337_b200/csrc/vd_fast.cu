@@ -13,6 +13,9 @@ bool try_group_k9(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, 
 bool try_group_k568(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe);
 bool try_punct_k7(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
                   std::int64_t* mi1);
+// vd_small.cu: 8-states-per-lane kernel for latency-bound small launches
+bool small_launch_wanted(const DecodeLaunch& p);
+bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err);
 
 // ---- run-time instantiations (vd_jit.cu) for other complement-paired codes --
 // plan() uses only K and B of its code, so one placeholder code per (K, B)
@@ -111,6 +114,7 @@ bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t strea
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream) {
   using namespace fast;
   cudaError_t err = cudaErrorNotSupported;
+  if (small_launch_wanted(p) && try_small(p, stream, &err)) return err;
   if (try_group_k7(p, stream, &err, false)) return err;
   if (try_group_k9(p, stream, &err, false)) return err;
   if (try_group_k568(p, stream, &err, false)) return err;

@@ -103,6 +103,12 @@ cudaError_t launch_count_bit_errors(const std::uint32_t* a, const std::uint32_t*
 /// launches of their timed region instead of assuming them.
 void note_launch(int n = 1);
 
+/// Dynamic shared-memory limit every kernel's cudaFuncAttributeMaxDynamic-
+/// SharedMemorySize is set to (sm_100 maximum per CTA). Always the maximum,
+/// never the launch's own size: host threads launching different geometries
+/// of one kernel at once must not lower the limit under each other.
+constexpr int kMaxDynSmem = 232448;
+
 /// SM count of the current device (cached per device).
 int sm_count();
 

@@ -421,3 +421,30 @@ def test_concurrent_host_calls_pageable_and_pinned(port):
         x.join()
     for (q, n, exp), got in zip(jobs, results):
         assert np.array_equal(got, exp)
+
+
+@pytest.mark.parametrize("polys", [[0o171, 0o133], [0o133, 0o171]])
+def test_small_launch_kernel_vs_oracle(polys, port, monkeypatch):
+    """Small launches (fewer 16-frame warps than schedulers) run the
+    8-states-per-lane kernel (csrc/vd_small_dev.cuh); bit-exact vs the oracle
+    and vs the 16-states-per-lane kernel (VITDEC_SMALL=0) over frame
+    configurations incl. subframe / random-start tracebacks, v1 not a multiple
+    of the 3-stage blocks, padded head frames and generic tail frames."""
+    k, b = 7, 2
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng(4242 + polys[0])
+    cfgs = [vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 45, 32), vd.FrameConfig(64, 16, 24, 16),
+            vd.FrameConfig(128, 20, 40, 32, vd.TracebackStart.kRandom, 5), vd.FrameConfig(100, 14, 30, 30),
+            vd.FrameConfig(512, 42, 42), vd.FrameConfig(32, 0, 35), vd.FrameConfig(96, 7, 11, 0)]
+    for i, cfg in enumerate(cfgs):
+        n = int(rng.integers(50_000, 400_000))
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(0, 4)), 300 + i)
+        q = oracle.quantize(rx, [32.0, 4.0][i % 2])
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        for small in ("1", "0"):
+            monkeypatch.setenv("VITDEC_SMALL", small)
+            packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+            got = vd.unpack_bits(packed, n)
+            bad = np.flatnonzero(got != exp)
+            assert bad.size == 0, (small, cfg, n, bad[:10], bad.size)
+            assert (stats.frames, stats.stages, stats.tracebacks) == st
