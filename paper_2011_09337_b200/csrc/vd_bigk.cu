@@ -248,7 +248,7 @@ cudaError_t launch_bigk(const DecodeLaunch& p, cudaStream_t stream) {
   bp.dec = reinterpret_cast<std::uint32_t*>(scratch + met_bytes * grid);
   auto kern = bigk_kernel<In, M>;
   cudaError_t e = cudaSuccess;
-  if (dyn > 0) e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  if (dyn > 0) e = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (e == cudaSuccess) {
     kern<<<static_cast<unsigned>(grid), kThreads, dyn, stream>>>(bp);
     note_launch();

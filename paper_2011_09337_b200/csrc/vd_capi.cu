@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -1056,6 +1057,20 @@ cudaError_t retain_async_pool() {
   std::uint64_t thr = ~0ull;
   if (cudaError_t e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr); e != cudaSuccess) return e;
   done[dev] = true;
+  return cudaSuccess;
+}
+
+cudaError_t allow_max_smem(const void* kern) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  if (cudaError_t e = cudaGetDevice(&dev); e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  if (cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+      e != cudaSuccess)
+    return e;
+  done.insert({kern, dev});
   return cudaSuccess;
 }
 

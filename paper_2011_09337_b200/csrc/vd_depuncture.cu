@@ -180,7 +180,7 @@ cudaError_t launch_depuncture_i8(const DepunctureLaunch& p, cudaStream_t stream)
   if ((reinterpret_cast<std::uintptr_t>(p.out) & 3u) != 0) return cudaErrorMisalignedAddress;
   const std::size_t smem = sizeof(uint2) * (p.unit_bytes / 4) + sizeof(std::uint32_t) * (p.tu * p.unit_in / 4 + 4);
   cudaError_t e =
-      cudaFuncSetAttribute(depuncture_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+      allow_max_smem(reinterpret_cast<const void*>(depuncture_kernel));
   if (e != cudaSuccess) return e;
   const std::int64_t tile_stages = static_cast<std::int64_t>(p.unit_periods) * p.period * p.tu;
   const std::int64_t tiles = (p.t0 + p.n - 1) / tile_stages - p.t0 / tile_stages + 1;

@@ -298,7 +298,7 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream, KSel ksel
   std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
   // (always the maximum: host threads launching different plans at once must
   // not lower the limit under each other's launches)
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return e;
   FastParams fpl = fp;
   // persistent grid: as many CTAs as are co-resident (one per SM with TMEM)
@@ -358,7 +358,7 @@ bool try_punct_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* 
   if (!stream && !err) return true;  // probe
   const FastParams& fp = pl.fp;
   auto kern = fast_kernel<C, R, true, false, PN>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (e == cudaSuccess) {
     const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
     std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;

@@ -586,7 +586,7 @@ cudaError_t launch_reg(GenericParams gp, cudaStream_t stream) {
   }
   const std::size_t smem = per_warp * kWarps;
   auto kern = reg_kernel<In, M, NPL, BT>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (e == cudaSuccess) {
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(gp);
     note_launch();
@@ -656,7 +656,7 @@ cudaError_t launch_generic(const DecodeLaunch& p, cudaStream_t stream) {
   }
   const std::size_t smem = per_warp * kWarps;
   auto kern = generic_kernel<In, M>;
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (e == cudaSuccess) {
     kern<<<static_cast<unsigned>(blocks), kWarps * 32, smem, stream>>>(gp);
     note_launch();

@@ -108,6 +108,10 @@ void note_launch(int n = 1);
 /// never the launch's own size: host threads launching different geometries
 /// of one kernel at once must not lower the limit under each other.
 constexpr int kMaxDynSmem = 232448;
+/// Sets kernel `kern`'s dynamic shared-memory limit to kMaxDynSmem on the
+/// current device, once per (kernel, device) (a driver call per launch costs
+/// microseconds of host time that small, latency-bound launches notice).
+cudaError_t allow_max_smem(const void* kern);
 
 /// SM count of the current device (cached per device).
 int sm_count();

@@ -17,24 +17,26 @@ constexpr int kSmallSmemMax = 232448;
 
 // Layout and grid for frames [mi0, mi1) that share one geometry (window L,
 // output length f_out).
-template <class C>
+template <class C, int R>
 bool plan_geom(const DecodeLaunch& p, std::int64_t mi0, std::int64_t mi1, int L, int f_out, SmallParams* out) {
-  using GEO = Geo<C, 8>;
+  using GEO = Geo<C, R>;
+  using SG = SmallGeo<R>;
   SmallParams sp{};
   sp.p = p;
   sp.m1 = 0xffffffffu;
   sp.L = L;
   sp.f_out = f_out;
-  sp.nsb = (L + 5) / 6;
+  sp.nsb = (L + SG::SB - 1) / SG::SB;
   sp.step = p.f0 > 0 ? p.f0 : p.f;
   sp.num_sub = (f_out + sp.step - 1) / sp.step;
-  if (sp.num_sub > 64 || L < 6 || 6 * sp.nsb > kSmallMaxStages || mi1 <= mi0) return false;
+  if (sp.num_sub > 64 || L < 6 || SG::SB * sp.nsb > kSmallMaxStages || mi1 <= mi0) return false;
   sp.mi0 = mi0;
   sp.mi1 = mi1;
   sp.safe_stage = (mi1 - 1) * p.f - p.v1;  // the last frame's window (empty slots)
   // per-warp shared memory: staged windows, survivor rows, relayout buffer, start states
-  sp.pitch = 12 * sp.nsb + 4;  // (+ 1 word: keeps the rows of different frames on different banks)
-  const int rows = 6 * sp.nsb - 6 * (p.v1 / 6) + 3;  // stages [6 floor(v1 / 6), 6 nsb) + traceback over-read
+  sp.pitch = 4 * SG::WSB * sp.nsb + 4;  // (+ 1 word: keeps the rows of different frames on different banks)
+  // survivor words: stages [SB floor(v1 / SB), SB nsb) + the traceback's over-read
+  const int rows = (SG::SB * sp.nsb - SG::SB * (p.v1 / SG::SB)) / SG::SPW + 3;
   sp.llr_off = 0;
   sp.dec_off = GEO::FPW * sp.pitch;
   sp.x_off = sp.dec_off + rows * 32 * 4;
@@ -61,9 +63,9 @@ struct SmallPlan {
   int ntail = 0;
 };
 
-template <class C>
+template <class C, int R>
 bool plan_small(const DecodeLaunch& p, SmallPlan* out) {
-  using GEO = Geo<C, 8>;
+  using GEO = Geo<C, R>;
   if (GEO::B != 2 || p.nblocks > 0 || p.sigma || p.frame_list) return false;
   SmallPlan pl;
   const int L = p.f + p.v1 + p.v2;
@@ -72,14 +74,14 @@ bool plan_small(const DecodeLaunch& p, SmallPlan* out) {
   const std::int64_t hi = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // full windows below
   const std::int64_t mi1 = std::min<std::int64_t>(hi, p.frame_end);
   if (mi1 > p.frame_begin) {
-    if (!plan_geom<C>(p, p.frame_begin, mi1, L, p.f, &pl.main)) return false;
+    if (!plan_geom<C, R>(p, p.frame_begin, mi1, L, p.f, &pl.main)) return false;
     pl.has_main = true;
   }
   for (std::int64_t m = std::max(mi1, p.frame_begin); m < p.frame_end; ++m) {
     if (pl.ntail == 4) return false;
     const FrameGeom g(m, p.n, p.f, p.v1, p.v2, p.f0);
     const std::int64_t ws = m * p.f - p.v1;  // virtual window start (zero-filled below stage 0)
-    if (!plan_geom<C>(p, m, m + 1, static_cast<int>(g.end - ws), static_cast<int>(g.out_hi - g.out_lo),
+    if (!plan_geom<C, R>(p, m, m + 1, static_cast<int>(g.end - ws), static_cast<int>(g.out_hi - g.out_lo),
                       &pl.tail[pl.ntail]))
       return false;
     ++pl.ntail;
@@ -89,22 +91,22 @@ bool plan_small(const DecodeLaunch& p, SmallPlan* out) {
   return true;
 }
 
-template <class C>
+template <class C, int R>
 cudaError_t launch_one(const SmallParams& sp, cudaStream_t stream) {
-  using GEO = Geo<C, 8>;
+  using GEO = Geo<C, R>;
   const std::int64_t warps = (sp.mi1 - sp.mi0 + GEO::FPW - 1) / GEO::FPW;
   const std::int64_t blocks = (warps + sp.warps_per_cta - 1) / sp.warps_per_cta;
   const std::size_t smem = static_cast<std::size_t>(sp.smem_per_warp) * sp.warps_per_cta;
   // (always the maximum: host threads launching different geometries at once
   // must not lower the limit under each other's launches)
-  cudaError_t e = cudaFuncSetAttribute(small_kernel<C>, cudaFuncAttributeMaxDynamicSharedMemorySize, kMaxDynSmem);
+  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(small_kernel<C, R>));
   if (e != cudaSuccess) return e;
-  small_kernel<C><<<static_cast<unsigned>(blocks), sp.warps_per_cta * 32, smem, stream>>>(sp);
+  small_kernel<C, R><<<static_cast<unsigned>(blocks), sp.warps_per_cta * 32, smem, stream>>>(sp);
   note_launch();
   return cudaGetLastError();
 }
 
-template <class C>
+template <class C, int R>
 cudaError_t launch_small(const SmallPlan& pl, cudaStream_t stream) {
   // tail frames (one warp each) on a side stream, concurrently with the main launch
   SideStream* side = nullptr;
@@ -114,12 +116,12 @@ cudaError_t launch_small(const SmallPlan& pl, cudaStream_t stream) {
     if (cudaError_t err = cudaEventRecord(side->fork, stream); err != cudaSuccess) return err;
     if (cudaError_t err = cudaStreamWaitEvent(side->s, side->fork, 0); err != cudaSuccess) return err;
     for (int i = 0; i < pl.ntail; ++i) {
-      if (cudaError_t err = launch_one<C>(pl.tail[i], side->s); err != cudaSuccess) return err;
+      if (cudaError_t err = launch_one<C, R>(pl.tail[i], side->s); err != cudaSuccess) return err;
     }
     if (cudaError_t err = cudaEventRecord(side->join, side->s); err != cudaSuccess) return err;
   }
   if (pl.has_main) {
-    if (cudaError_t err = launch_one<C>(pl.main, stream); err != cudaSuccess) return err;
+    if (cudaError_t err = launch_one<C, R>(pl.main, stream); err != cudaSuccess) return err;
   }
   if (side) return cudaStreamWaitEvent(stream, side->join, 0);
   return cudaSuccess;
@@ -139,13 +141,13 @@ bool small_launch_wanted(const DecodeLaunch& p) {
 bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
   SmallPlan pl;
   if (K7a::matches(p.k, p.b, p.polys)) {
-    if (!plan_small<K7a>(p, &pl)) return false;
-    *err = launch_small<K7a>(pl, stream);
+    if (!plan_small<K7a, 8>(p, &pl)) return false;
+    *err = launch_small<K7a, 8>(pl, stream);
     return true;
   }
   if (K7b::matches(p.k, p.b, p.polys)) {
-    if (!plan_small<K7b>(p, &pl)) return false;
-    *err = launch_small<K7b>(pl, stream);
+    if (!plan_small<K7b, 8>(p, &pl)) return false;
+    *err = launch_small<K7b, 8>(pl, stream);
     return true;
   }
   return false;

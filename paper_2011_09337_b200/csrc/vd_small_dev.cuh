@@ -48,18 +48,60 @@ struct SmallParams {
 constexpr int kSmallMaxWarps = 8;
 constexpr int kSmallMaxStages = 1032;  // largest staged window (f + v1 + v2 rounded up to 6 stages)
 
-// bit of (register rho, half h) in a survivor word of the small kernel
-__device__ __forceinline__ std::uint32_t small_bit(std::uint32_t rho, std::uint32_t hsh) {
-  return (rho & 3u) | ((rho & 4u) << 1) | hsh;
+// Geometry of the small kernel for R states per lane. Launched with R = 8;
+// R = 4 (16 lanes per frame pair, 4 frames per warp) is parity-clean but was
+// measured slower on C1 (19.5 vs 25.6 Gbps: the per-lane table and relayout
+// work no longer halves, profiles/r02_ab_notes.md).
+// Survivor-word layout of SmallGeo<R>: a stage's 2R decisions (R registers x
+// 2 frames) are merged by Q = R / 2 PRMTs (registers q and q + Q) and IMADs
+// into bit (rho % Q) + Q p + 8 (rho / Q) + 16 half, p = the stage's index
+// among the SPW stages that share the word.
+template <int R>
+struct SmallGeo {
+  static constexpr int LB = R == 8 ? 3 : 2;        // in-register stages between relayouts
+  static constexpr int SB = LB % 2 ? 2 * LB : LB;  // stages per super-block (whole LLR words at B = 2)
+  static constexpr int WSB = SB * 2 / 4;           // LLR words per frame and super-block
+  static constexpr int Q = R / 2;                  // PRMTs per stage
+  static constexpr int SPW = R == 8 ? 1 : 2;       // stages per survivor word (16 bits used each)
+  static_assert(SB % SPW == 0, "survivor words must not straddle super-blocks");
+  // bit index of register rho (p = 0), half h
+  __device__ static __forceinline__ std::uint32_t bit(std::uint32_t rho, std::uint32_t hsh) {
+    return (rho & (Q - 1)) | ((rho / Q) << 3) | hsh;
+  }
+  // bit of register bit j in that index: j < LB - 1 -> j, the top bit -> 3
+  static constexpr std::uint32_t pos(int j) { return j < LB - 1 ? j : 3u; }
+  // register index back from a bit index
+  __device__ static __forceinline__ std::uint32_t reg(std::uint32_t bx) {
+    return (bx & (Q - 1)) | (((bx >> 3) & 1u) << (LB - 1));
+  }
+};
+
+template <int I, int N, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (I < N) {
+    f(std::integral_constant<int, I>{});
+    static_for<I + 1, N>(f);
+  }
 }
 
-template <class C>
+// acc += y[q] * (0x01010101 << (q + Q ph)) for the Q PRMTs of one stage
+template <int Q, int PH, int q = 0>
+__device__ __forceinline__ void small_merge(const std::uint32_t* w, std::uint32_t& acc) {
+  if constexpr (q < Q) {
+    acc = mad_imm<(0x01010101u << (q + Q * PH))>(prmt(w[q], w[q + Q], 0xFBD9u), acc);
+    small_merge<Q, PH, q + 1>(w, acc);
+  }
+}
+
+template <class C, int R_>
 __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const SmallParams sp) {
-  using GEO = Geo<C, 8>;
+  using GEO = Geo<C, R_>;
+  using SG = SmallGeo<R_>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, R = GEO::R, r = GEO::r, g = GEO::g;
   constexpr int B = GEO::B, FPW = GEO::FPW;
-  static_assert(B == 2, "small kernel: rate-1/2 codes (12 LLR bytes per 6-stage super-block)");
-  static_assert(LB == 3 && R == 8, "small kernel geometry");
+  constexpr int SB = SG::SB, WSB = SG::WSB, Q = SG::Q, SPW = SG::SPW;
+  static_assert(B == 2, "small kernel: rate-1/2 codes");
+  static_assert(LB == SG::LB && (R == 8 || R == 4), "small kernel geometry");
   constexpr std::uint32_t BASE = 0x20002000u;
   constexpr std::uint32_t XM = C::kXM;
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * B) * 0x00010001u;
@@ -102,13 +144,14 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
   };
 
   // ---- stage the FPW frames' windows into shared memory (zero past L) -------
-  // Lane q handles frame slot q / 4 and every 4th word of its row, 16 words
-  // per chunk: a chunk's global loads are all issued before its stores (one
-  // memory latency per chunk); a window starting on an odd stage (byte offset
-  // 2) is re-aligned with one PRMT per word.
+  // LPS = 32 / FPW lanes per frame slot, each taking every LPS-th word of its
+  // row, 16 words per chunk (40: more registers, a slower stage loop): a
+  // chunk's global loads are all issued before its stores (one memory latency
+  // per chunk); a window starting on an odd stage
+  // (byte offset 2) is re-aligned with one PRMT per word.
   {
-    constexpr int kChunk = 16;
-    const int fs = lane >> 2, sub = lane & 3;
+    constexpr int kChunk = 16, LPS = 32 / FPW;
+    const int fs = lane / LPS, sub = lane % LPS;
     const bool v = mbase + fs < sp.mi1;
     const Slot sl = frame_slot(mbase + fs, v);
     // head frames (window start before stage 0 of the stream) read zeros
@@ -132,17 +175,17 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
       return e - 2 <= avail ? static_cast<std::uint32_t>(__ldg(reinterpret_cast<const std::uint16_t*>(w + i))) : 0u;
     };
     std::uint32_t* row = reinterpret_cast<std::uint32_t*>(llr_s + fs * pitch);
-    for (int c0 = 0; c0 < nw; c0 += 4 * kChunk) {
+    for (int c0 = 0; c0 < nw; c0 += LPS * kChunk) {
       std::uint32_t lo[kChunk], hi[kChunk];
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
-        const int i = c0 + sub + 4 * j;
+        const int i = c0 + sub + LPS * j;
         lo[j] = (i >= ifirst && 4 * i - mis < nbytes) ? ld(i) : 0u;
         hi[j] = (mis && i + 1 >= ifirst && 4 * i + 2 < nbytes) ? ld(i + 1) : 0u;
       }
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
-        const int i = c0 + sub + 4 * j;
+        const int i = c0 + sub + LPS * j;
         std::uint32_t x = mis ? prmt(lo[j], hi[j], 0x5432u) : lo[j];
         const int nb = nbytes - 4 * i;  // window bytes in this word
         x = nb >= 4 ? x : (nb > 0 ? (x & 0xffffu) : 0u);
@@ -153,13 +196,15 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
   __syncwarp();
 
   // ---- per-lane constants: LLR sign flips of the lane part of the branch
-  // index (phase k = stage % 3 of each of the super-block's 6 stages)
-  std::uint32_t fw[3];
-  std::uint32_t kc[6][2];
+  // index (phase k = stage % LB of each of the super-block's SB stages)
+  std::uint32_t fw[WSB];
+  std::uint32_t kc[SB][2];
   {
-    std::uint32_t w[3] = {0x80808080u, 0x80808080u, 0x80808080u};
+    std::uint32_t w[WSB];
 #pragma unroll
-    for (int k6 = 0; k6 < 6; ++k6) {
+    for (int j = 0; j < WSB; ++j) w[j] = 0x80808080u;
+#pragma unroll
+    for (int k6 = 0; k6 < SB; ++k6) {
       const int k = k6 % LB;
       std::uint32_t z = 0;
 #pragma unroll
@@ -174,7 +219,7 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
       kc[k6][1] = opaque((256u + phi0 - phi1) * 0x00010001u);
     }
 #pragma unroll
-    for (int j = 0; j < 3; ++j) fw[j] = opaque(w[j]);
+    for (int j = 0; j < WSB; ++j) fw[j] = opaque(w[j]);
   }
   const std::uint32_t m1 = opaque(sp.m1);
   std::uint32_t sig[R];
@@ -246,32 +291,33 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
 
   const std::uint32_t* rowA = reinterpret_cast<const std::uint32_t*>(llr_s + (2 * grp) * pitch);
   const std::uint32_t* rowB = reinterpret_cast<const std::uint32_t*>(llr_s + (2 * grp + 1) * pitch);
-  // Survivor rows: every stage of the super-blocks that hold a stage >= v1
-  // (rows from stage t_first = 6 * floor(v1 / 6)), so the stores need no range
-  // checks (the traceback reads only stages in [v1, L), decoder.cpp:229-235).
-  const int sb_warm = v1 / 6;  // super-blocks entirely before stage v1
-  const int t_first = 6 * sb_warm;
-  std::uint32_t* const drow = dec + lane - t_first * 32;
+  // Survivor rows (one word per SPW stages): every stage of the super-blocks
+  // that hold a stage >= v1 (from stage t_first = SB * floor(v1 / SB)), so the
+  // stores need no range checks (the traceback reads only stages in [v1, L),
+  // decoder.cpp:229-235).
+  const int sb_warm = v1 / SB;  // super-blocks entirely before stage v1
+  const int t_first = SB * sb_warm;
+  std::uint32_t* const drow = dec + lane - (t_first / SPW) * 32;
 
-  // One 6-stage super-block, straight-line: STORE keeps decision words; REC
+  // One SB-stage super-block, straight-line: STORE keeps decision words; REC
   // checks every stage for a stored-max start stage (only the super-blocks
   // that hold one).
   auto super_block = [&](int sb, auto store_tag, auto rec_tag) {
     constexpr bool STORE = decltype(store_tag)::value;
     constexpr bool REC = decltype(rec_tag)::value;
-    // tables of the 6 stages for both frames (reference decoder.cpp:22-51):
+    // tables of the SB stages for both frames (reference decoder.cpp:22-51):
     // PT[k][x] = T_k[x ^ lane part] + 256 per half
-    std::uint32_t il[3][2];
+    std::uint32_t il[WSB][2];
 #pragma unroll
-    for (int j = 0; j < 3; ++j) {
-      const std::uint32_t a = rowA[sb * 3 + j] ^ fw[j];
-      const std::uint32_t bq = rowB[sb * 3 + j] ^ fw[j];
+    for (int j = 0; j < WSB; ++j) {
+      const std::uint32_t a = rowA[sb * WSB + j] ^ fw[j];
+      const std::uint32_t bq = rowB[sb * WSB + j] ^ fw[j];
       il[j][0] = prmt(a, bq, 0x5410u);
       il[j][1] = prmt(a, bq, 0x7632u);
     }
-    std::uint32_t PT[6][4];
+    std::uint32_t PT[SB][4];
 #pragma unroll
-    for (int k6 = 0; k6 < 6; ++k6) {
+    for (int k6 = 0; k6 < SB; ++k6) {
       const int q0 = k6 * 2, q1 = k6 * 2 + 1;
       const std::uint32_t x0 = prmt(il[q0 >> 2][(q0 >> 1) & 1], 0u, (q0 & 1) ? 0x4341u : 0x4240u);
       const std::uint32_t x1 = prmt(il[q1 >> 2][(q1 >> 1) & 1], 0u, (q1 & 1) ? 0x4341u : 0x4240u);
@@ -283,12 +329,15 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
     std::uint32_t PA0[4];
 #pragma unroll
     for (int x = 0; x < 4; ++x) PA0[x] = __vadd2(PT[0][x], corr);  // renormalisation, folded
-#pragma unroll
-    for (int k6 = 0; k6 < 6; ++k6) {
-      const int k = k6 % LB;
-      const int t = sb * 6 + k6;
+    std::uint32_t acc = 0u;  // survivor word being merged (SPW stages)
+    static_for<0, SB>([&](auto k6c) {
+      constexpr int k6 = decltype(k6c)::value;
+      constexpr int k = k6 % LB;
+      const int t = sb * SB + k6;
       auto pa = [&](std::uint32_t x) { return k6 == 0 ? PA0[x] : PT[k6][x]; };
       std::uint32_t w[R];
+      (void)t;
+      (void)w;
 #pragma unroll
       for (int e = 0; e < R; ++e) {
         if ((e >> k) & 1) continue;
@@ -307,17 +356,16 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
         sig[od] = nH;
       }
       if constexpr (STORE) {
-        // 16 decisions -> one word (see compact16): y[q] = 255 * N_q
-        std::uint32_t acc = m1;
-        acc = mad_imm<0x01010101u>(prmt(w[0], w[4], 0xFBD9u), acc);
-        acc = mad_imm<0x02020202u>(prmt(w[1], w[5], 0xFBD9u), acc);
-        acc = mad_imm<0x04040404u>(prmt(w[2], w[6], 0xFBD9u), acc);
-        acc = mad_imm<0x08080808u>(prmt(w[3], w[7], 0xFBD9u), acc);
-        drow[t * 32] = acc;
+        // 2R decisions -> the word's Q bits of this stage (see compact16):
+        // y[q] = 255 * N_q, merged at bit q + Q p of each byte
+        constexpr int ph = k6 % SPW;
+        if constexpr (ph == 0) acc = m1;
+        small_merge<Q, ph>(w, acc);
+        if constexpr (ph == SPW - 1) drow[(t / SPW) * 32] = acc;
       }
       if constexpr (REC) rec(t, k);
-      if (k == LB - 1) relayout();
-    }
+      if constexpr (k == LB - 1) relayout();
+    });
     // renormalisation after every super-block (group-wide reference)
     const std::uint32_t ref = __shfl_sync(kFull, sig[0], grp * G);
     corr = __vsub2(BASE, ref);
@@ -367,8 +415,9 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
     const std::uint32_t P0 = ((state << sh) | (state >> (M - sh))) & GEO::SMASK;
     const std::uint32_t hsh = half ? 16u : 0u;
     std::uint32_t lp = P0 >> r;
-    std::uint32_t Bx = small_bit(P0 & (R - 1), hsh);
-    const std::uint32_t* dcol = dec + (fr >> 1) * G - t_first * 32;  // dcol[t * 32 + lp]: word of stage t
+    std::uint32_t Bx = SG::bit(P0 & (R - 1), hsh);
+    // word of stage t: dcol[(t / SPW) * 32 + lp], its bits at + Q (t % SPW)
+    const std::uint32_t* dcol = dec + (fr >> 1) * G - (t_first / SPW) * 32;
     const std::int64_t obase = sl.ws - p.out_stage0;
     std::uint64_t acc = 0;  // emitted bits, lowest stage at bit 0
     int nb = 0;
@@ -392,29 +441,29 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
       }
     };
     // register bits of the bit index at block entry -> decoded bits of the block
-    auto block_bits = [](std::uint32_t bx) { return (bx & 3u) | ((bx >> 1) & 4u); };
+    auto block_bits = [](std::uint32_t bx) { return SG::reg(bx); };
     // the relayout undone: P -> rotl(P, r) for the block below
     auto next_block = [&]() {
       const std::uint32_t P = (lp << r) | block_bits(Bx);
       const std::uint32_t Pn = ((P << r) | (P >> (M - r))) & GEO::SMASK;
       lp = Pn >> r;
-      Bx = small_bit(Pn & (R - 1), hsh);
+      Bx = SG::bit(Pn & (R - 1), hsh);
     };
-    // one step at phase j of the block starting at stage tb0
+    // one step at phase j of a block (blocks start at multiples of LB, so the
+    // stage's position in its survivor word is j % SPW)
     auto step_j = [&](std::uint32_t word, int j) {
-      constexpr std::uint32_t kPos[3] = {0u, 1u, 3u};
-      const std::uint32_t pos = j == 0 ? kPos[0] : j == 1 ? kPos[1] : kPos[2];
-      const std::uint32_t x = __funnelshift_r(word, word, Bx - pos);  // bit Bx -> bit pos
+      const std::uint32_t pos = SG::pos(j);
+      const std::uint32_t x = __funnelshift_r(word, word, Bx + Q * (j % SPW) - pos);  // bit -> bit pos
       Bx = bitsel_m(x, Bx, 1u << pos);
     };
     int tb0 = st_t - st_t % LB;
-    // top block: phases st_t % 3 .. max(sub_lo - tb0, 0)
+    // top block: phases st_t % LB .. max(sub_lo - tb0, 0)
     {
       const int jhi = st_t - tb0, jlo = max(sub_lo - tb0, 0);
       const std::uint32_t bin = block_bits(Bx);
 #pragma unroll
       for (int j = LB - 1; j >= 0; --j) {
-        if (j <= jhi && j >= jlo) step_j(dcol[(tb0 + j) * 32 + lp], j);
+        if (j <= jhi && j >= jlo) step_j(dcol[((tb0 + j) / SPW) * 32 + lp], j);
       }
       const int ehi = min(jhi, sub_hi - 1 - tb0);
       if (ehi >= jlo) emit(tb0 + jlo, ehi - jlo + 1, (bin >> jlo) & ((1u << (ehi - jlo + 1)) - 1u));
@@ -423,12 +472,13 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
     }
     // whole blocks above sub_lo
     for (; tb0 >= sub_lo; tb0 -= LB) {
-      const std::uint32_t* src = dcol + tb0 * 32 + lp;
-      const std::uint32_t w0 = src[0], w1 = src[32], w2 = src[64];
+      const std::uint32_t* src = dcol + (tb0 / SPW) * 32 + lp;
+      std::uint32_t wd[LB];
+#pragma unroll
+      for (int j = 0; j < LB; ++j) wd[j] = src[(j / SPW) * 32];
       const std::uint32_t bin = block_bits(Bx);
-      step_j(w2, 2);
-      step_j(w1, 1);
-      step_j(w0, 0);
+#pragma unroll
+      for (int j = LB - 1; j >= 0; --j) step_j(wd[j], j);
       if (tb0 + LB <= sub_hi) {
         emit(tb0, LB, bin);
       } else if (tb0 < sub_hi) {
