@@ -21,6 +21,9 @@ value: device-timed (CUDA events on the decode stream, max over ranks)
 e2e:   the same metric through the reference-facing host call
        (vd_decode_i8: pinned host LLRs -> H2D -> kernel -> D2H packed bits,
        streamed in chunks; each rank its 1/N share), timed around the call.
+e2e_reference_api (N = 1, C5): the reference's own C++ signature,
+       vitdec::framed_decode(LlrBlock of doubles) -> bytes, 2^26 bits
+       (tools/bench_dropin.cpp): conversion, staging and unpack included.
 roofline: the decode kernel against its binding roof (integer ALU: the
        measured ACS-pair rate of profiles/alu_peak.json, and the dual-issue
        bound; the HBM roof alongside), see DESIGN.md §4. traffic: DRAM bytes
@@ -277,6 +280,26 @@ def kernel_traffic(workload: str):
     if not w:
         return None, None
     return w["bytes_per_bit"], d.get("source")
+
+
+def dropin_e2e(args):
+    """End to end through the reference-facing C++ call itself,
+    vitdec::framed_decode(LlrBlock of doubles) -> std::vector<uint8_t> bits
+    (paper_2011_09337_b200/bench_dropin, tools/bench_dropin.cpp): includes the
+    integer check / double -> int8 conversion, pageable staging and the byte
+    unpack that the native int8 call of `e2e` skips. Secondary to `e2e`."""
+    exe = ROOT / "paper_2011_09337_b200" / "bench_dropin"
+    if not exe.exists():
+        return None
+    n = 1 << 26
+    try:
+        r = subprocess.run([str(exe), str(n), "3"], capture_output=True, text=True, timeout=600)
+        d = json.loads(r.stdout.strip().splitlines()[-1])
+    except Exception as e:  # noqa: BLE001 - report, do not fail the headline line
+        return {"unavailable": f"{type(e).__name__}: {e}"[:200]}
+    d["path"] = ("vitdec::framed_decode(const LlrBlock&, ...) C++ drop-in: B x N doubles in, bytes out, "
+                 "host conversion + pageable staging + H2D + decode + D2H + unpack timed per call (median)")
+    return d
 
 
 def run_ours(args):
@@ -556,6 +579,9 @@ def run_ours(args):
         }
         if weak:
             result["weak_scaling"] = weak
+        api = dropin_e2e(args) if world == 1 and args.e2e_steps > 0 and args.workload == "C5" else None
+        if api is not None:
+            result["e2e_reference_api"] = api
         print(json.dumps(result))
     if dist:
         dist.barrier()

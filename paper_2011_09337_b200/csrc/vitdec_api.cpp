@@ -14,6 +14,8 @@
 #include <thread>
 #include <vector>
 
+#include <cuda_runtime.h>
+
 #include "vitdec/decoder.hpp"
 #include "vitdec/trellis.hpp"
 #include "vitdec_b200.h"
@@ -88,27 +90,64 @@ void host_parallel(std::int64_t n, int workers, Fn&& fn) {
   for (auto& t : th) t.join();
 }
 
+// Per-thread pinned host buffers for the converted int8 block and the packed
+// result of the drop-in framed_decode: H2D / D2H go straight from / to them
+// (no staging copy) and repeated calls reuse them (no fresh pages per call).
+// Grown on demand; plain heap memory when pinned memory is unavailable.
+struct HostScratch {
+  void* p[2] = {nullptr, nullptr};
+  std::size_t cap[2] = {0, 0};
+  bool pinned[2] = {false, false};
+  ~HostScratch() {
+    for (int i = 0; i < 2; ++i) release(i);
+  }
+  void release(int i) {
+    if (!p[i]) return;
+    if (pinned[i]) {
+      cudaFreeHost(p[i]);
+    } else {
+      std::free(p[i]);
+    }
+    p[i] = nullptr;
+    cap[i] = 0;
+  }
+  void* get(int i, std::size_t bytes) {
+    if (cap[i] >= bytes) return p[i];
+    release(i);
+    const std::size_t want = std::max<std::size_t>(bytes, cap[i] + cap[i] / 2);
+    pinned[i] = cudaMallocHost(&p[i], want) == cudaSuccess;
+    if (!pinned[i]) {
+      cudaGetLastError();
+      p[i] = std::malloc(want);
+      if (!p[i]) throw std::bad_alloc();
+    }
+    cap[i] = want;
+    return p[i];
+  }
+};
+thread_local HostScratch t_scratch;
+
 // Integer-valued blocks in [-127, 127] decode exactly on the int8 kernels.
-bool int8_exact(const LlrBlock& llr, std::vector<std::int8_t>* q, int workers) {
+bool int8_exact(const LlrBlock& llr, std::int8_t* out, int workers) {
   const Eigen::Index n = llr.size();
-  q->resize(static_cast<std::size_t>(n));
   const double* d = llr.data();
-  std::int8_t* out = q->data();
   std::atomic<bool> ok{true};
   host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
-    bool good = true;
-    for (std::int64_t i = lo; i < hi; ++i) {  // branch-free body: vectorisable
+    int bad = 0;
+    for (std::int64_t i = lo; i < hi; ++i) {  // branch-free, no libm rounding call
       const double v = d[i];
-      const double r = std::nearbyint(v);
-      good &= (v >= -127.0) & (v <= 127.0) & (r == v);
-      out[i] = static_cast<std::int8_t>(good ? r : 0.0);
+      // clamp (NaN -> -127), truncate: v is an integer in [-127, 127] iff the
+      // truncated value equals it
+      const int iv = static_cast<int>(std::fmin(std::fmax(v, -127.0), 127.0));
+      bad |= static_cast<double>(iv) != v;
+      out[i] = static_cast<std::int8_t>(iv);
     }
-    if (!good) ok.store(false, std::memory_order_relaxed);
+    if (bad) ok.store(false, std::memory_order_relaxed);
   });
   return ok.load();
 }
 
-BitVec unpack(const std::vector<std::uint32_t>& packed, Eigen::Index n, int workers = 1) {
+BitVec unpack(const std::uint32_t* packed, Eigen::Index n, int workers = 1) {
   BitVec bits(static_cast<std::size_t>(n));
   host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
     for (std::int64_t i = lo; i < hi; ++i) bits[i] = static_cast<std::uint8_t>((packed[i >> 5] >> (i & 31)) & 1u);
@@ -236,16 +275,16 @@ DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const Fr
   cfg.validate();
   const vd_frame_cfg c = to_c(cfg);
   const Eigen::Index n = llr.cols();
-  std::vector<std::uint32_t> packed(static_cast<std::size_t>((n + 31) / 32));
+  auto* packed = static_cast<std::uint32_t*>(t_scratch.get(1, sizeof(std::uint32_t) * static_cast<std::size_t>((n + 31) / 32)));
   vd_stats st{};
   vd_exec ex{};
   ex.num_devices = env_gpus();
-  std::vector<std::int8_t> q;
+  auto* q = static_cast<std::int8_t*>(t_scratch.get(0, static_cast<std::size_t>(llr.size())));
   // `workers` host threads prepare the block / unpack the bits (the GPU does the decode)
-  if (int8_exact(llr, &q, workers)) {
-    check(vd_decode_i8(trellis.native(), &c, q.data(), n, packed.data(), &st, &ex));
+  if (int8_exact(llr, q, workers)) {
+    check(vd_decode_i8(trellis.native(), &c, q, n, packed, &st, &ex));
   } else {
-    check(vd_decode_f64(trellis.native(), &c, llr.data(), n, packed.data(), &st, &ex));
+    check(vd_decode_f64(trellis.native(), &c, llr.data(), n, packed, &st, &ex));
   }
   DecodeOutput out;
   out.bits = unpack(packed, n, workers);
@@ -258,8 +297,8 @@ DecodeOutput serial_decode(const LlrBlock& llr, const Trellis& trellis) {
   const Eigen::Index n = llr.cols();
   std::vector<std::uint32_t> packed(static_cast<std::size_t>((n + 31) / 32));
   vd_stats st{};
-  std::vector<std::int8_t> q;
-  if (n <= 0x7fffffff && int8_exact(llr, &q, 1)) {
+  std::vector<std::int8_t> q(static_cast<std::size_t>(llr.size()));
+  if (n <= 0x7fffffff && int8_exact(llr, q.data(), 1)) {
     // One frame covering the block with no overlap == serial_decode
     // (reference acceptance.cpp:57-81 equivalence).
     vd_frame_cfg c{};
@@ -271,7 +310,7 @@ DecodeOutput serial_decode(const LlrBlock& llr, const Trellis& trellis) {
     check(vd_serial_decode_f64(trellis.native(), llr.data(), n, packed.data(), &st, -1));
   }
   DecodeOutput out;
-  out.bits = unpack(packed, n);
+  out.bits = unpack(packed.data(), n);
   out.stats = from_c(st);
   return out;
 }
