@@ -292,10 +292,8 @@ vd_status decode_device(const vd_code* code, const vd_frame_cfg* cfg, std::int64
   cudaStream_t s = static_cast<cudaStream_t>(stream);
 
   VD_CUDA(vd::retain_async_pool(), "memory pool");
-  // Zero the output words the frames touch; kernels OR bits into them.
   const std::int64_t w0 = (g0.out_lo - out_stage0) / 32;
   const std::int64_t w1 = (g1.out_hi - out_stage0 + 31) / 32;
-  VD_CUDA(cudaMemsetAsync(out + w0, 0, sizeof(std::uint32_t) * (w1 - w0), s), "zero output");
 
   vd::DecodeLaunch p;
   p.k = code->k;
@@ -318,6 +316,12 @@ vd_status decode_device(const vd_code* code, const vd_frame_cfg* cfg, std::int64
   p.in_out = in_out;
   for (int i = 0; i < code->b && i < 8; ++i) p.polys[i] = code->polys[i];
   p.complement_paired = code->complement_paired;
+
+  // Zero the output words the frames touch (kernels OR bits into them),
+  // unless the launch writes every word whole.
+  bool whole = false;
+  if constexpr (sizeof(T) == 1) whole = vd::fast_output_whole_words(p);
+  if (!whole) VD_CUDA(cudaMemsetAsync(out + w0, 0, sizeof(std::uint32_t) * (w1 - w0), s), "zero output");
 
   cudaError_t e;
   if constexpr (sizeof(T) == 1) {

@@ -16,6 +16,7 @@ bool try_punct_k7(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaE
 // vd_small.cu: 8-states-per-lane kernel for latency-bound small launches
 bool small_launch_wanted(const DecodeLaunch& p);
 bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err);
+bool small_writes_whole_words(const DecodeLaunch& p);
 
 // ---- run-time instantiations (vd_jit.cu) for other complement-paired codes --
 // plan() uses only K and B of its code, so one placeholder code per (K, B)
@@ -109,6 +110,10 @@ bool fast_path_supported(const DecodeLaunch& p) {
 bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err,
                           std::int64_t* mi0, std::int64_t* mi1) {
   return fast::try_punct_k7(p, pattern, stream, err, mi0, mi1);
+}
+
+bool fast_output_whole_words(const DecodeLaunch& p) {
+  return fast_path_supported(p) && fast::small_writes_whole_words(p);
 }
 
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream) {

@@ -31,6 +31,10 @@ constexpr int kPfSlackStages = 12;
 /// code/config is outside its envelope (caller then uses the generic one).
 bool fast_path_supported(const DecodeLaunch& p);
 cudaError_t launch_fast_i8(const DecodeLaunch& p, cudaStream_t stream);
+/// True when launch_fast_i8(p) writes every output word of its frames whole
+/// (the small-launch kernel with 32-aligned frame / subframe boundaries): the
+/// caller may then skip zeroing the output.
+bool fast_output_whole_words(const DecodeLaunch& p);
 /// Fused depuncture (pattern 23: "11;10", 34: "110;101"; B = 2 codes with a
 /// fused instantiation): p.llr is the punctured stream; launches the fast
 /// kernel over the interior frames [*mi0, *mi1) it takes (stream == nullptr

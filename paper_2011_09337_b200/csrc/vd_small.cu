@@ -42,89 +42,75 @@ bool plan_geom(const DecodeLaunch& p, std::int64_t mi0, std::int64_t mi1, int L,
   sp.x_off = sp.dec_off + rows * 32 * 4;
   sp.ss_off = sp.x_off + GEO::GROUPS * GEO::XSTRIDE * 4;
   sp.smem_per_warp = (sp.ss_off + GEO::FPW * sp.num_sub * 2 + 15) & ~15;
-  const std::int64_t warps = (mi1 - mi0 + GEO::FPW - 1) / GEO::FPW;
-  const int sms = sm_count();
-  int wpc = static_cast<int>(std::min<std::int64_t>((warps + sms - 1) / sms, kSmallMaxWarps));
-  wpc = std::max(wpc, 1);
-  while (wpc > 1 && sp.smem_per_warp * wpc > kSmallSmemMax) --wpc;
-  if (sp.smem_per_warp * wpc > kSmallSmemMax) return false;
-  sp.warps_per_cta = wpc;
   *out = sp;
   return true;
 }
 
-// The launch's frames: [mi0, mi1) with the full window (interior and, when the
-// buffer starts at stage 0, head frames), then every clipped tail frame with
-// its own geometry (FrameGeom, reference decoder.cpp:175-191).
-struct SmallPlan {
-  SmallParams main;
-  bool has_main = false;
-  SmallParams tail[4];
-  int ntail = 0;
-};
-
+// The launch's frames in segments: [frame_begin, mi1) with the full window
+// (interior and, when the buffer starts at stage 0, head frames), then every
+// clipped tail frame with its own geometry (FrameGeom, reference
+// decoder.cpp:175-191), all in ONE launch (the tail frames' warps run on other
+// SMs beside the main segment's; no side stream, no events).
 template <class C, int R>
-bool plan_small(const DecodeLaunch& p, SmallPlan* out) {
+bool plan_small(const DecodeLaunch& p, SmallLaunch* out) {
   using GEO = Geo<C, R>;
   if (GEO::B != 2 || p.nblocks > 0 || p.sigma || p.frame_list) return false;
-  SmallPlan pl;
+  SmallLaunch sl{};
   const int L = p.f + p.v1 + p.v2;
   const std::int64_t lo = p.llr_stage0 == 0 ? 0 : (p.llr_stage0 + p.v1 + p.f - 1) / p.f;
   if (std::max(lo, p.frame_begin) != p.frame_begin) return false;  // windows before the buffer
   const std::int64_t hi = (p.n - p.f - p.v2 >= 0) ? (p.n - p.f - p.v2) / p.f + 1 : 0;  // full windows below
   const std::int64_t mi1 = std::min<std::int64_t>(hi, p.frame_end);
-  if (mi1 > p.frame_begin) {
-    if (!plan_geom<C, R>(p, p.frame_begin, mi1, L, p.f, &pl.main)) return false;
-    pl.has_main = true;
-  }
+  std::int64_t warps = 0;
+  int smem = 0;
+  auto add = [&](std::int64_t m0, std::int64_t m1, int len, int f_out) {
+    if (sl.nseg == kSmallSegs) return false;
+    SmallParams& sp = sl.seg[sl.nseg];
+    if (!plan_geom<C, R>(p, m0, m1, len, f_out, &sp)) return false;
+    sl.warp_begin[sl.nseg] = static_cast<int>(warps);
+    warps += (m1 - m0 + GEO::FPW - 1) / GEO::FPW;
+    smem = std::max(smem, sp.smem_per_warp);
+    ++sl.nseg;
+    return true;
+  };
+  if (mi1 > p.frame_begin && !add(p.frame_begin, mi1, L, p.f)) return false;
   for (std::int64_t m = std::max(mi1, p.frame_begin); m < p.frame_end; ++m) {
-    if (pl.ntail == 4) return false;
     const FrameGeom g(m, p.n, p.f, p.v1, p.v2, p.f0);
     const std::int64_t ws = m * p.f - p.v1;  // virtual window start (zero-filled below stage 0)
-    if (!plan_geom<C, R>(p, m, m + 1, static_cast<int>(g.end - ws), static_cast<int>(g.out_hi - g.out_lo),
-                      &pl.tail[pl.ntail]))
-      return false;
-    ++pl.ntail;
+    if (!add(m, m + 1, static_cast<int>(g.end - ws), static_cast<int>(g.out_hi - g.out_lo))) return false;
   }
-  if (!pl.has_main && pl.ntail == 0) return false;
-  *out = pl;
+  if (sl.nseg == 0 || warps > (1 << 30)) return false;
+  sl.warp_begin[sl.nseg] = static_cast<int>(warps);
+  const int sms = sm_count();
+  int wpc = static_cast<int>(std::min<std::int64_t>((warps + sms - 1) / sms, kSmallMaxWarps));
+  wpc = std::max(wpc, 1);
+  while (wpc > 1 && smem * wpc > kSmallSmemMax) --wpc;
+  if (smem * wpc > kSmallSmemMax) return false;
+  sl.warps_per_cta = wpc;
+  sl.smem_per_warp = smem;
+  // every output word written whole by one task: frame and subframe
+  // boundaries on 32-bit words (frame m's output starts at m * f), and a
+  // stream end inside the launch on one too (tasks emit from their top stage
+  // down, so a subframe ending at n must span whole words)
+  const int step = p.f0 > 0 ? p.f0 : p.f;
+  const bool ends_in = p.frame_end * static_cast<std::int64_t>(p.f) >= p.n;
+  sl.whole_words = p.f % 32 == 0 && step % 32 == 0 && p.out_stage0 % 32 == 0 && (!ends_in || p.n % 32 == 0);
+  *out = sl;
   return true;
 }
 
 template <class C, int R>
-cudaError_t launch_one(const SmallParams& sp, cudaStream_t stream) {
-  using GEO = Geo<C, R>;
-  const std::int64_t warps = (sp.mi1 - sp.mi0 + GEO::FPW - 1) / GEO::FPW;
-  const std::int64_t blocks = (warps + sp.warps_per_cta - 1) / sp.warps_per_cta;
-  const std::size_t smem = static_cast<std::size_t>(sp.smem_per_warp) * sp.warps_per_cta;
+cudaError_t launch_small(const SmallLaunch& sl, cudaStream_t stream) {
+  const std::int64_t warps = sl.warp_begin[sl.nseg];
+  const std::int64_t blocks = (warps + sl.warps_per_cta - 1) / sl.warps_per_cta;
+  const std::size_t smem = static_cast<std::size_t>(sl.smem_per_warp) * sl.warps_per_cta;
   // (always the maximum: host threads launching different geometries at once
   // must not lower the limit under each other's launches)
   cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(small_kernel<C, R>));
   if (e != cudaSuccess) return e;
-  small_kernel<C, R><<<static_cast<unsigned>(blocks), sp.warps_per_cta * 32, smem, stream>>>(sp);
+  small_kernel<C, R><<<static_cast<unsigned>(blocks), sl.warps_per_cta * 32, smem, stream>>>(sl);
   note_launch();
   return cudaGetLastError();
-}
-
-template <class C, int R>
-cudaError_t launch_small(const SmallPlan& pl, cudaStream_t stream) {
-  // tail frames (one warp each) on a side stream, concurrently with the main launch
-  SideStream* side = nullptr;
-  if (pl.ntail > 0) {
-    side = side_stream();
-    if (!side) return cudaErrorUnknown;
-    if (cudaError_t err = cudaEventRecord(side->fork, stream); err != cudaSuccess) return err;
-    if (cudaError_t err = cudaStreamWaitEvent(side->s, side->fork, 0); err != cudaSuccess) return err;
-    for (int i = 0; i < pl.ntail; ++i) {
-      if (cudaError_t err = launch_one<C, R>(pl.tail[i], side->s); err != cudaSuccess) return err;
-    }
-    if (cudaError_t err = cudaEventRecord(side->join, side->s); err != cudaSuccess) return err;
-  }
-  if (pl.has_main) {
-    if (cudaError_t err = launch_one<C, R>(pl.main, stream); err != cudaSuccess) return err;
-  }
-  if (side) return cudaStreamWaitEvent(stream, side->join, 0);
-  return cudaSuccess;
 }
 
 }  // namespace
@@ -138,19 +124,32 @@ bool small_launch_wanted(const DecodeLaunch& p) {
   return warps16 < static_cast<std::int64_t>(sm_count()) * 4;
 }
 
-bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
-  SmallPlan pl;
-  if (K7a::matches(p.k, p.b, p.polys)) {
-    if (!plan_small<K7a, 8>(p, &pl)) return false;
-    *err = launch_small<K7a, 8>(pl, stream);
+// Which small-kernel plan serves p (nullptr: none); fills *sl.
+bool plan_any(const DecodeLaunch& p, SmallLaunch* sl, int* code) {
+  if (K7a::matches(p.k, p.b, p.polys) && plan_small<K7a, 8>(p, sl)) {
+    *code = 0;
     return true;
   }
-  if (K7b::matches(p.k, p.b, p.polys)) {
-    if (!plan_small<K7b, 8>(p, &pl)) return false;
-    *err = launch_small<K7b, 8>(pl, stream);
+  if (K7b::matches(p.k, p.b, p.polys) && plan_small<K7b, 8>(p, sl)) {
+    *code = 1;
     return true;
   }
   return false;
+}
+
+bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
+  SmallLaunch sl;
+  int code = -1;
+  if (!plan_any(p, &sl, &code)) return false;
+  *err = code == 0 ? launch_small<K7a, 8>(sl, stream) : launch_small<K7b, 8>(sl, stream);
+  return true;
+}
+
+bool small_writes_whole_words(const DecodeLaunch& p) {
+  if (!small_launch_wanted(p)) return false;
+  SmallLaunch sl;
+  int code = -1;
+  return plan_any(p, &sl, &code) && sl.whole_words;
 }
 
 }  // namespace fast

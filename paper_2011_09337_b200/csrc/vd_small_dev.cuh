@@ -37,8 +37,7 @@ struct SmallParams {
   int f_out;              // output stages per frame (f, or a partial last frame's)
   int nsb;                // 6-stage super-blocks per frame
   int step, num_sub;      // subframe geometry
-  int warps_per_cta;
-  int smem_per_warp;      // bytes per warp
+  int smem_per_warp;      // bytes per warp this geometry needs
   int llr_off, dec_off, x_off, ss_off;  // regions of a warp's area
   int pitch;              // bytes per staged frame row (multiple of 12, >= 12 * nsb)
   std::int64_t safe_stage;      // window start of an interior frame (empty slots)
@@ -46,6 +45,21 @@ struct SmallParams {
 };
 
 constexpr int kSmallMaxWarps = 8;
+constexpr int kSmallSegs = 4;  // frame segments per launch: the full-window frames + up to 3 clipped tail frames
+
+// One launch: segment i (its own window / output geometry) owns the grid's
+// warps [warp_begin[i], warp_begin[i + 1]); every warp's area is the largest
+// segment's. whole_words: every output word belongs to one traceback task
+// (32-aligned frame and subframe boundaries), so the host skips zeroing the
+// output and partial last words are stored, not OR-ed.
+struct SmallLaunch {
+  SmallParams seg[kSmallSegs];
+  int warp_begin[kSmallSegs + 1];
+  int nseg;
+  int warps_per_cta;
+  int smem_per_warp;
+  int whole_words;
+};
 constexpr int kSmallMaxStages = 1032;  // largest staged window (f + v1 + v2 rounded up to 6 stages)
 
 // Geometry of the small kernel for R states per lane. Launched with R = 8;
@@ -94,7 +108,7 @@ __device__ __forceinline__ void small_merge(const std::uint32_t* w, std::uint32_
 }
 
 template <class C, int R_>
-__global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const SmallParams sp) {
+__global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const SmallLaunch sl_) {
   using GEO = Geo<C, R_>;
   using SG = SmallGeo<R_>;
   constexpr int M = GEO::M, S = GEO::S, G = GEO::G, LB = GEO::LB, R = GEO::R, r = GEO::r, g = GEO::g;
@@ -105,7 +119,6 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
   constexpr std::uint32_t BASE = 0x20002000u;
   constexpr std::uint32_t XM = C::kXM;
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * B) * 0x00010001u;
-  const DecodeLaunch& p = sp.p;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // (opaque: keeps the lane-derived values in registers instead of
@@ -114,14 +127,18 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
   const int warp = threadIdx.x >> 5;
   const int grp = lane / G;
   const int lam = lane % G;
-  unsigned char* wbase = smem_raw + static_cast<std::size_t>(warp) * sp.smem_per_warp;
+  unsigned char* wbase = smem_raw + static_cast<std::size_t>(warp) * sl_.smem_per_warp;
+  const int gwarp = static_cast<int>(blockIdx.x) * sl_.warps_per_cta + warp;
+  int si = 0;
+  while (si + 1 < sl_.nseg && gwarp >= sl_.warp_begin[si + 1]) ++si;
+  const SmallParams& sp = sl_.seg[si];
+  const DecodeLaunch& p = sp.p;
   unsigned char* llr_s = wbase + sp.llr_off;
   std::uint32_t* dec = reinterpret_cast<std::uint32_t*>(wbase + sp.dec_off);
   std::uint32_t* xbuf = reinterpret_cast<std::uint32_t*>(wbase + sp.x_off);
   std::uint16_t* sstate = reinterpret_cast<std::uint16_t*>(wbase + sp.ss_off);
 
-  const std::int64_t gwarp = static_cast<std::int64_t>(blockIdx.x) * sp.warps_per_cta + warp;
-  const std::int64_t mbase = sp.mi0 + gwarp * FPW;
+  const std::int64_t mbase = sp.mi0 + static_cast<std::int64_t>(gwarp - sl_.warp_begin[si]) * FPW;
   if (mbase >= sp.mi1) return;
 
   const int f = static_cast<int>(opaque(static_cast<std::uint32_t>(p.f)));
@@ -499,8 +516,12 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
       const std::int64_t ol = obase + sub_lo;
       const std::int64_t w0 = ol >> 5;
       const int o = static_cast<int>(ol & 31);
-      atomicOr(p.out + w0, word << o);
-      if (o + nb > 32) atomicOr(p.out + w0 + 1, word >> (32 - o));
+      if (o == 0 && sl_.whole_words) {
+        p.out[w0] = word;  // the stream's last, partial word: ours alone
+      } else {
+        atomicOr(p.out + w0, word << o);
+        if (o + nb > 32) atomicOr(p.out + w0 + 1, word >> (32 - o));
+      }
     }
   }
 }

@@ -448,3 +448,31 @@ def test_small_launch_kernel_vs_oracle(polys, port, monkeypatch):
             bad = np.flatnonzero(got != exp)
             assert bad.size == 0, (small, cfg, n, bad[:10], bad.size)
             assert (stats.frames, stats.stages, stats.tracebacks) == st
+
+
+@pytest.mark.parametrize("cfg", [(256, 20, 20, 0), (320, 20, 45, 32), (256, 20, 20, 0, 7)],
+                         ids=["f256", "f320f0_32", "n_unaligned"])
+def test_small_launch_whole_words_over_stale_output(cfg, port):
+    """Small launches with 32-aligned frame / subframe boundaries write every
+    output word whole and skip the output zeroing: an output buffer full of
+    stale ones must come back exactly equal to the oracle's bits (an unaligned
+    stream end keeps the zeroing)."""
+    import torch
+
+    from paper_2011_09337_b200.device import decode_i8_device
+
+    f, v1, v2, f0 = cfg[:4]
+    n = 3200 * 32 + (cfg[4] if len(cfg) > 4 else 0)
+    k, b, polys = K7
+    rx, _ = port.gen_bench_block(k, b, polys, n, 2.5, 99 + f)
+    q = oracle.quantize(rx, 32.0)
+    exp, _, _ = port.framed_decode(k, b, polys, q, n, f, v1, v2, f0)
+    t = trellis(k, b, polys)
+    fc = vd.FrameConfig(f, v1, v2, f0)
+    nf = -(-n // f)
+    llr = torch.from_numpy(q).cuda()
+    out = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+    decode_i8_device(t, fc, n, llr, 0, 0, nf, out, 0)
+    torch.cuda.synchronize()
+    got = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
+    assert np.array_equal(got, exp), np.flatnonzero(got != exp)[:10]
