@@ -40,8 +40,9 @@ bool try_jit_kb(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bo
 }
 
 // The fast kernel's envelope: 5 <= K <= 9 (16 states per lane; int16 metric
-// range), B in {2, 3}, every polynomial tapping the newest
-// and the oldest register bit (both butterfly edges are complement pairs).
+// range), B in {2, 3}; any polynomials (complement-paired or
+// not: a butterfly's four edge labels are x, x ^ cb(0), x ^ cb(K-1) and
+// x ^ cb(0) ^ cb(K-1), all compile-time).
 bool jit_code(const DecodeLaunch& p) { return jit::enabled() && fast_envelope_code(p.k, p.b, p.polys); }
 
 bool try_jit(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe) {
@@ -92,11 +93,8 @@ cudaError_t launch_head_gather(const std::int8_t* llr, const std::int64_t* blk_s
 }
 
 bool fast_envelope_code(int k, int b, const std::uint32_t* polys) {
-  if (k < 5 || k > 9 || (b != 2 && b != 3)) return false;
-  for (int i = 0; i < b; ++i) {
-    if (!(polys[i] & 1u) || !((polys[i] >> (k - 1)) & 1u)) return false;
-  }
-  return true;
+  (void)polys;  // any generator polynomials: the edge labels are compile-time per code
+  return k >= 5 && k <= 9 && (b == 2 || b == 3);
 }
 
 bool fast_path_supported(const DecodeLaunch& p) {

@@ -532,7 +532,7 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
                                           const std::uint32_t* pfA, const std::uint32_t* pfB, std::uint32_t sA,
                                           RecFn&& rec) {
   constexpr int LB = GEO::LB, R = GEO::R, WPB = GEO::WPB;
-  constexpr std::uint32_t XM = C::kXM;
+  constexpr std::uint32_t CB0 = C::cb(0), CBT = C::cb(C::kK - 1);
   // ---- branch-metric tables for the LB stages of this block (both frames) ---
   std::uint32_t PT[LB][1 << GEO::B];
   block_tables<C, GEO, BUF>(st, PT);
@@ -578,10 +578,13 @@ __device__ __forceinline__ void run_block(FrameState<GEO>& st, int blk, const Bl
       const int od = e | (1 << k);
       const std::uint32_t x = GEO::xreg(k, e);
       const std::uint32_t sE = st.sig[e], sO = st.sig[od];
-      const std::uint32_t s2L = __vadd2(sO, pa(k, x ^ XM));
-      const std::uint32_t s2H = __vadd2(sO, pa(k, x));
+      // edge labels (reference trellis.cpp:65-91, in_out): E -> L is x; the
+      // odd predecessor adds cb(0), input 1 (the H state) adds cb(K - 1)
+      // (both XM for complement-paired codes)
+      const std::uint32_t s2L = __vadd2(sO, pa(k, x ^ CB0));
+      const std::uint32_t s2H = __vadd2(sO, pa(k, x ^ CB0 ^ CBT));
       const std::uint32_t nL = __viaddmax_s16x2(sE, pa(k, x), s2L);
-      const std::uint32_t nH = __viaddmax_s16x2(sE, pa(k, x ^ XM), s2H);
+      const std::uint32_t nH = __viaddmax_s16x2(sE, pa(k, x ^ CBT), s2H);
       // Decision words: bit 15 / 31 set iff the FIRST predecessor won, i.e.
       // s1 - s2 >= 1 per half (ties -> second, decoder.cpp:67-74); + 0x7FFF
       // per half keeps each half in [0, 0xFFFE], so no carry crosses halves.

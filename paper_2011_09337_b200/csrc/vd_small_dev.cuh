@@ -118,6 +118,7 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
   static_assert(LB == SG::LB && (R == 8 || R == 4), "small kernel geometry");
   constexpr std::uint32_t BASE = 0x20002000u;
   constexpr std::uint32_t XM = C::kXM;
+  constexpr std::uint32_t CB0 = C::cb(0), CBT = C::cb(C::kK - 1);
   constexpr std::uint32_t OFFB = static_cast<std::uint32_t>(256 * B) * 0x00010001u;
 
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -361,10 +362,10 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
         const int od = e | (1 << k);
         const std::uint32_t x = GEO::xreg(k, e);
         const std::uint32_t sE = sig[e], sO = sig[od];
-        const std::uint32_t s2L = __vadd2(sO, pa(x ^ XM));
-        const std::uint32_t s2H = __vadd2(sO, pa(x));
+        const std::uint32_t s2L = __vadd2(sO, pa(x ^ CB0));  // edge labels: see run_block
+        const std::uint32_t s2H = __vadd2(sO, pa(x ^ CB0 ^ CBT));
         const std::uint32_t nL = __viaddmax_s16x2(sE, pa(x), s2L);
-        const std::uint32_t nH = __viaddmax_s16x2(sE, pa(x ^ XM), s2H);
+        const std::uint32_t nH = __viaddmax_s16x2(sE, pa(x ^ CBT), s2H);
         if constexpr (STORE) {
           w[e] = nL - s2L + 0x7fff7fffu;  // bit 15 / 31: the first predecessor won
           w[od] = nH - s2H + 0x7fff7fffu;

@@ -3,9 +3,9 @@ precompiled list (csrc/vd_jit.cu).
 
 The reference's ACS is code-generic through the trellis tables
 (proj/src/decoder.cpp:53-76, trellis.cpp:57-100); the fast kernel bakes the
-polynomials into compile-time table selections, so every complement-paired
-code with 5 <= K <= 9 and B in {2, 3} gets its own instantiation compiled on
-first use. CPU tests: the envelope and the NVRTC compile of the embedded
+polynomials into compile-time table selections, so every code with
+5 <= K <= 9 and B in {2, 3} (complement-paired or not) gets its own
+instantiation compiled on first use. CPU tests: the envelope and the NVRTC compile of the embedded
 sources (no GPU needed). GPU tests: bit-exact parity with the oracle and
 identical results with the JIT disabled (generic kernel).
 """
@@ -15,7 +15,9 @@ import pytest
 import oracle
 import paper_2011_09337_b200 as vd
 
-# complement-paired codes that are NOT among the precompiled instantiations
+# codes that are NOT among the precompiled instantiations: complement-paired
+# ones, and ones whose polynomials miss the newest or the oldest tap (their
+# butterfly edges are not complement pairs: four distinct edge labels)
 JIT_CODES = [
     (7, 2, [0o165, 0o117]),
     (7, 3, [0o171, 0o133, 0o145]),
@@ -23,6 +25,9 @@ JIT_CODES = [
     (6, 2, [0o65, 0o57]),
     (8, 3, [0o225, 0o331, 0o367]),
     (9, 2, [0o657, 0o435]),
+    (7, 2, [0o170, 0o133]),         # not paired: 0170 misses the oldest tap
+    (5, 2, [0o22, 0o35]),           # not paired
+    (8, 2, [0o247, 0o170]),         # not paired: neither edge bit is common
 ]
 
 
@@ -35,11 +40,9 @@ def test_jit_envelope(monkeypatch):
     lib = vd.lib()
     for spec in JIT_CODES:
         assert trellis(spec).fast_path(), spec
-    # not complement-paired (0170 misses the oldest tap) -> generic kernel
-    t = trellis((7, 2, [0o170, 0o133]))
-    assert not t.fast_path()
+    # K outside 5..9 -> generic kernel
+    t = trellis((4, 2, [0o17, 0o13]))
     assert lib.vd_code_jit_check(t.handle) == vd.api.VD_EUNSUPPORTED
-    # K outside 5..9
     assert not trellis((4, 2, [0o17, 0o13])).fast_path()
     assert not trellis((10, 2, [0o1157, 0o1753])).fast_path()
     monkeypatch.setenv("VITDEC_JIT", "0")
