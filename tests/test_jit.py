@@ -84,3 +84,36 @@ def test_jit_fast_path_vs_oracle(spec, monkeypatch, tmp_path):
             packed0, _ = vd.framed_decode_stream(q, n, t, cfg)
             assert np.array_equal(vd.unpack_bits(packed0, n), exp)
             monkeypatch.delenv("VITDEC_JIT")
+
+
+@pytest.mark.gpu
+def test_jit_concurrent_first_use(monkeypatch, tmp_path):
+    """Several host threads decoding codes that need a run-time instantiation
+    at the same moment (first use of each, one shared per-process cache):
+    every thread gets its code's kernel and the oracle's bits."""
+    import threading
+
+    monkeypatch.setenv("VITDEC_JIT_CACHE", str(tmp_path))
+    port = oracle.port()
+    specs = [(7, 2, [0o117, 0o165]), (6, 2, [0o57, 0o65]), (7, 2, [0o117, 0o165]), (9, 2, [0o435, 0o657])]
+    cfg = vd.FrameConfig(256, 20, 20)
+    jobs, res = [], [None] * len(specs)
+    for i, (k, b, polys) in enumerate(specs):
+        n = 80_000 + 999 * i
+        rx, _ = port.gen_bench_block(k, b, polys, n, 2.5, 500 + i)
+        q = oracle.quantize(rx)
+        exp, _, _ = port.framed_decode(k, b, polys, q, n, 256, 20, 20)
+        jobs.append((trellis((k, b, polys)), q, n, exp))
+
+    def run(i):
+        t, q, n, _ = jobs[i]
+        packed, _ = vd.framed_decode_stream(q, n, t, cfg)
+        res[i] = vd.unpack_bits(packed, n)
+
+    th = [threading.Thread(target=run, args=(i,)) for i in range(len(jobs))]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for (_, _, _, exp), got in zip(jobs, res):
+        assert got is not None and np.array_equal(got, exp)
