@@ -80,7 +80,8 @@ def parse():
     ap.add_argument("--no-weak", action="store_true", help="skip the secondary weak-scaling line (N > 1)")
     ap.add_argument("--frame", default="", help="f,v1,v2[,f0] frame configuration override (default 256,20,20)")
     ap.add_argument("--polys", default="", help="octal generator polynomials overriding the workload's code "
-                    "(same K and B; e.g. 165,117: a code served by a run-time kernel instantiation)")
+                    "(same B; e.g. 165,117: a code served by a run-time kernel instantiation)")
+    ap.add_argument("--k", type=int, default=0, help="constraint length for --polys (0: the workload's)")
     a = ap.parse_args()
     if a.frame:
         global F, V1, V2, F0
@@ -90,6 +91,7 @@ def parse():
     a.code, default_n, a.workload_desc = WORKLOADS[a.workload]
     if a.polys:
         k, b, _ = a.code
+        k = a.k or k
         polys = [int(x, 8) for x in a.polys.split(",")]
         if len(polys) != b or any(p >> k for p in polys):
             raise SystemExit(f"--polys needs {b} polynomials of at most K={k} bits")

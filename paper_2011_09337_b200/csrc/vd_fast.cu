@@ -39,8 +39,8 @@ bool try_jit_kb(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bo
   return true;
 }
 
-// The fast kernel's envelope: 5 <= K <= 9 (16 states per lane; int16 metric
-// range), B in {2, 3}; any polynomials (complement-paired or
+// The fast kernel's envelope: 5 <= K <= 10 (16 states per lane, at most 32
+// lanes per frame pair; int16 metric range), B in {2, 3}; any polynomials (complement-paired or
 // not: a butterfly's four edge labels are x, x ^ cb(0), x ^ cb(K-1) and
 // x ^ cb(0) ^ cb(K-1), all compile-time).
 bool jit_code(const DecodeLaunch& p) { return jit::enabled() && fast_envelope_code(p.k, p.b, p.polys); }
@@ -58,6 +58,8 @@ bool try_jit(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool 
     case 83: return try_jit_kb<8, 3>(p, stream, err, probe);
     case 92: return try_jit_kb<9, 2>(p, stream, err, probe);
     case 93: return try_jit_kb<9, 3>(p, stream, err, probe);
+    case 102: return try_jit_kb<10, 2>(p, stream, err, probe);
+    case 103: return try_jit_kb<10, 3>(p, stream, err, probe);
     default: return false;
   }
 }
@@ -94,7 +96,7 @@ cudaError_t launch_head_gather(const std::int8_t* llr, const std::int64_t* blk_s
 
 bool fast_envelope_code(int k, int b, const std::uint32_t* polys) {
   (void)polys;  // any generator polynomials: the edge labels are compile-time per code
-  return k >= 5 && k <= 9 && (b == 2 || b == 3);
+  return k >= 5 && k <= 10 && (b == 2 || b == 3);
 }
 
 bool fast_path_supported(const DecodeLaunch& p) {

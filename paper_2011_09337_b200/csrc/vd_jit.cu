@@ -1,6 +1,6 @@
 // Run-time instantiation of the fast kernel for codes outside the
 // precompiled list (vd_fast_k*.cu): any rate-1/2 or 1/3 code with
-// 5 <= K <= 9 (complement-paired, reference Trellis::complement_paired,
+// 5 <= K <= 10 (complement-paired, reference Trellis::complement_paired,
 // trellis.cpp:93-100, or not). The kernel bakes the polynomials into compile-time
 // table selections (vd_fast_dev.cuh, Geo::xreg / xlane), so a new code needs
 // a new instantiation: NVRTC compiles vd_fast_dev.cuh (embedded in this

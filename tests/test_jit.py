@@ -4,7 +4,7 @@ precompiled list (csrc/vd_jit.cu).
 The reference's ACS is code-generic through the trellis tables
 (proj/src/decoder.cpp:53-76, trellis.cpp:57-100); the fast kernel bakes the
 polynomials into compile-time table selections, so every code with
-5 <= K <= 9 and B in {2, 3} (complement-paired or not) gets its own
+5 <= K <= 10 and B in {2, 3} (complement-paired or not) gets its own
 instantiation compiled on first use. CPU tests: the envelope and the NVRTC compile of the embedded
 sources (no GPU needed). GPU tests: bit-exact parity with the oracle and
 identical results with the JIT disabled (generic kernel).
@@ -28,6 +28,8 @@ JIT_CODES = [
     (7, 2, [0o170, 0o133]),         # not paired: 0170 misses the oldest tap
     (5, 2, [0o22, 0o35]),           # not paired
     (8, 2, [0o247, 0o170]),         # not paired: neither edge bit is common
+    (10, 2, [0o1157, 0o1753]),      # K = 10: 32 lanes per frame pair, 2 frames per warp
+    (10, 3, [0o1157, 0o1753, 0o1331]),
 ]
 
 
@@ -44,7 +46,7 @@ def test_jit_envelope(monkeypatch):
     t = trellis((4, 2, [0o17, 0o13]))
     assert lib.vd_code_jit_check(t.handle) == vd.api.VD_EUNSUPPORTED
     assert not trellis((4, 2, [0o17, 0o13])).fast_path()
-    assert not trellis((10, 2, [0o1157, 0o1753])).fast_path()
+    assert not trellis((11, 2, [0o2335, 0o3277])).fast_path()
     monkeypatch.setenv("VITDEC_JIT", "0")
     assert not trellis(JIT_CODES[0]).fast_path()
     assert trellis((7, 2, [0o171, 0o133])).fast_path()  # precompiled: unaffected
