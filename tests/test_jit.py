@@ -119,3 +119,26 @@ def test_jit_concurrent_first_use(monkeypatch, tmp_path):
         x.join()
     for (_, _, _, exp), got in zip(jobs, res):
         assert got is not None and np.array_equal(got, exp)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", [(10, 3, [0o1157, 0o1753, 0o1331]), (10, 2, [0o1157, 0o1753]),
+                                  (9, 3, [0o557, 0o663, 0o711])], ids=["K10B3", "K10B2", "K9B3"])
+def test_metric_range_at_saturated_llrs(spec, monkeypatch, tmp_path):
+    """The int16 metric range at its extreme: every LLR +-127 (random signs and
+    a long all-+127 run), K = 10 / 9 with B = 3 (the largest spread the fast
+    kernel admits), bit-exact vs the oracle."""
+    monkeypatch.setenv("VITDEC_JIT_CACHE", str(tmp_path))
+    k, b, polys = spec
+    rng = np.random.default_rng(k * 100 + b)
+    n = 120_000
+    q = rng.choice(np.array([-127, 127], np.int8), size=n * b)
+    q[: 3000 * b] = 127
+    port = oracle.port()
+    t = trellis(spec)
+    assert t.fast_path()
+    for cfg in (vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 45, 32)):
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0)
+        packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+        got = vd.unpack_bits(packed, n)
+        assert np.array_equal(got, exp), (spec, cfg, np.flatnonzero(got != exp)[:10])
