@@ -94,6 +94,7 @@ void host_parallel(std::int64_t n, int workers, Fn&& fn) {
 // result of the drop-in framed_decode: H2D / D2H go straight from / to them
 // (no staging copy) and repeated calls reuse them (no fresh pages per call).
 // Grown on demand; plain heap memory when pinned memory is unavailable.
+constexpr std::size_t kMaxPinned = std::size_t{512} << 20;
 struct HostScratch {
   void* p[2] = {nullptr, nullptr};
   std::size_t cap[2] = {0, 0};
@@ -115,7 +116,9 @@ struct HostScratch {
     if (cap[i] >= bytes) return p[i];
     release(i);
     const std::size_t want = std::max<std::size_t>(bytes, cap[i] + cap[i] / 2);
-    pinned[i] = cudaMallocHost(&p[i], want) == cudaSuccess;
+    // (pinned up to kMaxPinned per buffer: larger blocks use pageable memory,
+    // which the library stages through its own pinned chunks)
+    pinned[i] = want <= kMaxPinned && cudaMallocHost(&p[i], want) == cudaSuccess;
     if (!pinned[i]) {
       cudaGetLastError();
       p[i] = std::malloc(want);
