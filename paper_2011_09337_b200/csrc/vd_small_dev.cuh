@@ -193,7 +193,27 @@ __global__ void __launch_bounds__(kSmallMaxWarps * 32, 1) small_kernel(const Sma
       return e - 2 <= avail ? static_cast<std::uint32_t>(__ldg(reinterpret_cast<const std::uint16_t*>(w + i))) : 0u;
     };
     std::uint32_t* row = reinterpret_cast<std::uint32_t*>(llr_s + fs * pitch);
-    for (int c0 = 0; c0 < nw; c0 += LPS * kChunk) {
+    // Common case, uniform over the warp: every window 4-byte aligned and
+    // wholly inside the stream -> plain loads, no per-word checks.
+    const bool simple = __all_sync(kFull, mis == 0 && sl.ws >= 0 && avail >= 4 * static_cast<std::int64_t>(nw));
+    if (simple) {
+      for (int c0 = 0; c0 < nw; c0 += LPS * kChunk) {
+        std::uint32_t x[kChunk];
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const int i = c0 + sub + LPS * j;
+          x[j] = i < nw ? __ldg(w + i) : 0u;
+        }
+#pragma unroll
+        for (int j = 0; j < kChunk; ++j) {
+          const int i = c0 + sub + LPS * j;
+          const int nb = nbytes - 4 * i;  // window bytes in this word
+          const std::uint32_t v = nb >= 4 ? x[j] : (nb > 0 ? (x[j] & 0xffffu) : 0u);
+          if (i < nw) row[i] = v;
+        }
+      }
+    }
+    for (int c0 = 0; c0 < (simple ? 0 : nw); c0 += LPS * kChunk) {
       std::uint32_t lo[kChunk], hi[kChunk];
 #pragma unroll
       for (int j = 0; j < kChunk; ++j) {
