@@ -80,7 +80,7 @@ def parse():
     ap.add_argument("--no-weak", action="store_true", help="skip the secondary weak-scaling line (N > 1)")
     ap.add_argument("--frame", default="", help="f,v1,v2[,f0] frame configuration override (default 256,20,20)")
     ap.add_argument("--polys", default="", help="octal generator polynomials overriding the workload's code "
-                    "(same B; e.g. 165,117: a code served by a run-time kernel instantiation)")
+                    "(B = their count; e.g. 165,117: a code served by a run-time kernel instantiation)")
     ap.add_argument("--k", type=int, default=0, help="constraint length for --polys (0: the workload's)")
     a = ap.parse_args()
     if a.frame:
@@ -90,11 +90,11 @@ def parse():
         F0 = vals[3] if len(vals) > 3 else 0
     a.code, default_n, a.workload_desc = WORKLOADS[a.workload]
     if a.polys:
-        k, b, _ = a.code
-        k = a.k or k
+        k = a.k or a.code[0]
         polys = [int(x, 8) for x in a.polys.split(",")]
-        if len(polys) != b or any(p >> k for p in polys):
-            raise SystemExit(f"--polys needs {b} polynomials of at most K={k} bits")
+        b = len(polys)  # rate 1/B from the polynomial count
+        if any(p >> k for p in polys):
+            raise SystemExit(f"--polys: polynomials of at most K={k} bits")
         a.code = (k, b, polys)
         a.workload_desc += f", code overridden: ({','.join(oct(p)[2:] for p in polys)})"
 

@@ -89,7 +89,7 @@ vd_status vd_code_tables(const vd_code* code, uint32_t* next, uint32_t* out, uin
                          int32_t* complement_paired);
 /* 1 when the fast register-resident kernel serves this code, else 0 (the
  * generic sm_100a kernel is used). Codes outside the precompiled list with
- * 5 <= K <= 10 and B in {2, 3} are served by a run-time (NVRTC) instantiation
+ * 5 <= K <= 10 and B in {2, 3, 4} are served by a run-time (NVRTC) instantiation
  * of the same kernel, compiled on first use and cached
  * (VITDEC_JIT=0 disables it, VITDEC_JIT_CACHE sets the cubin cache dir). */
 int32_t vd_code_fast_path(const vd_code* code);

@@ -1180,7 +1180,7 @@ int32_t vd_code_fast_path(const vd_code* code) {
 vd_status vd_code_jit_check(const vd_code* code) {
   if (!code) return fail(VD_EINVAL, "null code");
   if (!vd::fast_envelope_code(code->k, code->b, code->polys.data()))
-    return fail(VD_EUNSUPPORTED, "code outside the fast kernel's envelope (5 <= K <= 10, B in {2, 3})");
+    return fail(VD_EUNSUPPORTED, "code outside the fast kernel's envelope (5 <= K <= 10, B in {2, 3, 4})");
   if (!vd::jit::compile_check(code->k, code->b, code->polys.data())) return fail(VD_ECUDA, vd::jit::last_log());
   return VD_OK;
 }

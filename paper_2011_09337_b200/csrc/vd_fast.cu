@@ -22,7 +22,8 @@ bool small_writes_whole_words(const DecodeLaunch& p);
 // plan() uses only K and B of its code, so one placeholder code per (K, B)
 // class plans every code of the class; the kernel comes from the JIT.
 template <int K, int B>
-using PlanCode = CodeB<K, B, (1u << (K - 1)) | 1u, (1u << (K - 1)) | 1u, B == 3 ? ((1u << (K - 1)) | 1u) : 0u>;
+using PlanCode = CodeB<K, B, (1u << (K - 1)) | 1u, (1u << (K - 1)) | 1u, B >= 3 ? ((1u << (K - 1)) | 1u) : 0u,
+                       B >= 4 ? ((1u << (K - 1)) | 1u) : 0u>;
 
 struct JitSel {
   const DecodeLaunch* p;
@@ -40,7 +41,7 @@ bool try_jit_kb(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bo
 }
 
 // The fast kernel's envelope: 5 <= K <= 10 (16 states per lane, at most 32
-// lanes per frame pair; int16 metric range), B in {2, 3}; any polynomials (complement-paired or
+// lanes per frame pair; int16 metric range), B in {2, 3, 4}; any polynomials (complement-paired or
 // not: a butterfly's four edge labels are x, x ^ cb(0), x ^ cb(K-1) and
 // x ^ cb(0) ^ cb(K-1), all compile-time).
 bool jit_code(const DecodeLaunch& p) { return jit::enabled() && fast_envelope_code(p.k, p.b, p.polys); }
@@ -60,6 +61,12 @@ bool try_jit(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool 
     case 93: return try_jit_kb<9, 3>(p, stream, err, probe);
     case 102: return try_jit_kb<10, 2>(p, stream, err, probe);
     case 103: return try_jit_kb<10, 3>(p, stream, err, probe);
+    case 54: return try_jit_kb<5, 4>(p, stream, err, probe);
+    case 64: return try_jit_kb<6, 4>(p, stream, err, probe);
+    case 74: return try_jit_kb<7, 4>(p, stream, err, probe);
+    case 84: return try_jit_kb<8, 4>(p, stream, err, probe);
+    case 94: return try_jit_kb<9, 4>(p, stream, err, probe);
+    case 104: return try_jit_kb<10, 4>(p, stream, err, probe);
     default: return false;
   }
 }
@@ -96,12 +103,12 @@ cudaError_t launch_head_gather(const std::int8_t* llr, const std::int64_t* blk_s
 
 bool fast_envelope_code(int k, int b, const std::uint32_t* polys) {
   (void)polys;  // any generator polynomials: the edge labels are compile-time per code
-  return k >= 5 && k <= 10 && (b == 2 || b == 3);
+  return k >= 5 && k <= 10 && b >= 2 && b <= 4;
 }
 
 bool fast_path_supported(const DecodeLaunch& p) {
   using namespace fast;
-  if (p.b != 2 && p.b != 3) return false;
+  if (p.b < 2 || p.b > 4) return false;
   cudaError_t unused = cudaSuccess;
   return try_group_k7(p, nullptr, &unused, true) || try_group_k9(p, nullptr, &unused, true) ||
          try_group_k568(p, nullptr, &unused, true) || try_jit(p, nullptr, &unused, true);

@@ -51,13 +51,13 @@ __device__ __forceinline__ std::uint32_t prmt(std::uint32_t a, std::uint32_t b, 
 
 constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v >> 1); }
 
-/// Rate-1/B code (B = 2 or 3) with compile-time generator polynomials.
-template <int K_, int B_, std::uint32_t P0, std::uint32_t P1, std::uint32_t P2 = 0>
+/// Rate-1/B code (B = 2, 3 or 4) with compile-time generator polynomials.
+template <int K_, int B_, std::uint32_t P0, std::uint32_t P1, std::uint32_t P2 = 0, std::uint32_t P3 = 0>
 struct CodeB {
   static constexpr int kK = K_;
   static constexpr int kB = B_;
   static constexpr std::uint32_t kXM = (1u << B_) - 1u;  // complement mask of a branch index
-  static constexpr std::uint32_t poly(int i) { return i == 0 ? P0 : i == 1 ? P1 : P2; }
+  static constexpr std::uint32_t poly(int i) { return i == 0 ? P0 : i == 1 ? P1 : i == 2 ? P2 : P3; }
   // Branch-index bits contributed by register bit q (poly 0 -> MSB of the
   // index, as reference trellis.cpp:70-73 packs branch outputs).
   static constexpr std::uint32_t cb(int q) {
@@ -419,7 +419,7 @@ struct FrameState {
   // negation), kc[k][e] are the per-phase corrections that make the one's
   // complement exact inside the table sums.
   std::uint32_t fw[GEO::WPB];
-  std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : 3];
+  std::uint32_t kc[GEO::LB][GEO::B == 2 ? 2 : GEO::B];
   std::uint32_t llr[2][2][GEO::WPB];  // [buffer][frame A/B][word]: even/odd blocks
   std::uint32_t m1_p;                 // -1 from the parameter bank
   std::uint32_t corr;                 // pending renormalisation (BASE - ref per half)
@@ -452,7 +452,7 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
     if constexpr (B == 2) {
       PT[k][0] = x0 + x1 + st.kc[k][0];             // l0 + l1 + 256
       PT[k][1] = x0 - x1 + st.kc[k][1];             // l0 - l1 + 256
-    } else {
+    } else if constexpr (B == 3) {
       const std::uint32_t x2 = X(k, 2) + st.kc[k][2];
       const std::uint32_t a = x0 + x1 + st.kc[k][0];  // l0 + l1 + 256
       const std::uint32_t d = x0 - x1 + st.kc[k][1];  // l0 - l1 + 256
@@ -460,6 +460,21 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
       PT[k][1] = a - x2 + 0x01000100u;
       PT[k][2] = d + x2;
       PT[k][3] = d - x2 + 0x01000100u;
+    } else {  // B = 4: T + 512 per half
+      const std::uint32_t a = x0 + x1 + st.kc[k][0];  // l0 + l1 + 256
+      const std::uint32_t d = x0 - x1 + st.kc[k][1];  // l0 - l1 + 256
+      const std::uint32_t x2 = X(k, 2) + st.kc[k][2];  // l2 + 128
+      const std::uint32_t x3 = X(k, 3) + st.kc[k][3];  // l3 + 128
+      const std::uint32_t pp = x2 + x3;                // l2 + l3 + 256
+      const std::uint32_t qq = x2 - x3;                // l2 - l3
+      PT[k][0] = a + pp;
+      PT[k][1] = a + qq + 0x01000100u;
+      PT[k][2] = a - qq + 0x01000100u;
+      PT[k][3] = a - pp + 0x02000200u;
+      PT[k][4] = d + pp;
+      PT[k][5] = d + qq + 0x01000100u;
+      PT[k][6] = d - qq + 0x01000100u;
+      PT[k][7] = d - pp + 0x02000200u;
     }
 #pragma unroll
     for (int x = 0; x < GEO::NT; ++x) {
@@ -798,7 +813,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       for (int i = 0; i < g; ++i) {
         if ((lam >> i) & 1) z ^= C::cb(r + i - k);
       }
-      std::uint32_t phi[3] = {0u, 0u, 0u};  // llr i negated for this lane
+      std::uint32_t phi[4] = {0u, 0u, 0u, 0u};  // llr i negated for this lane
 #pragma unroll
       for (int i = 0; i < B; ++i) {
         phi[i] = (z >> (B - 1 - i)) & 1u;
@@ -808,7 +823,8 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       // one's complement (255 - u) is the exact negation (256 - u) minus 1
       st.kc[k][0] = opaque((phi[0] + phi[1]) * 0x00010001u);
       st.kc[k][1] = opaque((256u + phi[0] - phi[1]) * 0x00010001u);
-      if constexpr (B == 3) st.kc[k][2] = opaque(phi[2] * 0x00010001u);
+      if constexpr (B >= 3) st.kc[k][2] = opaque(phi[2] * 0x00010001u);
+      if constexpr (B == 4) st.kc[k][3] = opaque(phi[3] * 0x00010001u);
     }
 #pragma unroll
     for (int j = 0; j < WPB; ++j) st.fw[j] = opaque(fw[j]);

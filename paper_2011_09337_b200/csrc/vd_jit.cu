@@ -1,5 +1,5 @@
 // Run-time instantiation of the fast kernel for codes outside the
-// precompiled list (vd_fast_k*.cu): any rate-1/2 or 1/3 code with
+// precompiled list (vd_fast_k*.cu): any rate-1/2, 1/3 or 1/4 code with
 // 5 <= K <= 10 (complement-paired, reference Trellis::complement_paired,
 // trellis.cpp:93-100, or not). The kernel bakes the polynomials into compile-time
 // table selections (vd_fast_dev.cuh, Geo::xreg / xlane), so a new code needs
@@ -178,8 +178,9 @@ const std::string& last_log() { return t_log; }
 
 std::string expression(int k, int b, const std::uint32_t* polys, bool tm, bool gl) {
   char buf[256];
-  std::snprintf(buf, sizeof(buf), "&vd::fast::fast_kernel<vd::fast::CodeB<%d, %d, %uu, %uu, %uu>, 16, %s, %s>", k, b,
-                polys[0], polys[1], b > 2 ? polys[2] : 0u, tm ? "true" : "false", gl ? "true" : "false");
+  std::snprintf(buf, sizeof(buf), "&vd::fast::fast_kernel<vd::fast::CodeB<%d, %d, %uu, %uu, %uu, %uu>, 16, %s, %s>", k,
+                b, polys[0], polys[1], b > 2 ? polys[2] : 0u, b > 3 ? polys[3] : 0u, tm ? "true" : "false",
+                gl ? "true" : "false");
   return buf;
 }
 

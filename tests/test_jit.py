@@ -4,7 +4,7 @@ precompiled list (csrc/vd_jit.cu).
 The reference's ACS is code-generic through the trellis tables
 (proj/src/decoder.cpp:53-76, trellis.cpp:57-100); the fast kernel bakes the
 polynomials into compile-time table selections, so every code with
-5 <= K <= 10 and B in {2, 3} (complement-paired or not) gets its own
+5 <= K <= 10 and B in {2, 3, 4} (complement-paired or not) gets its own
 instantiation compiled on first use. CPU tests: the envelope and the NVRTC compile of the embedded
 sources (no GPU needed). GPU tests: bit-exact parity with the oracle and
 identical results with the JIT disabled (generic kernel).
@@ -30,6 +30,8 @@ JIT_CODES = [
     (8, 2, [0o247, 0o170]),         # not paired: neither edge bit is common
     (10, 2, [0o1157, 0o1753]),      # K = 10: 32 lanes per frame pair, 2 frames per warp
     (10, 3, [0o1157, 0o1753, 0o1331]),
+    (9, 4, [0o765, 0o671, 0o513, 0o473]),   # rate 1/4, K = 9 (cdma2000 r1/4)
+    (7, 4, [0o117, 0o127, 0o155, 0o171]),
 ]
 
 
@@ -123,11 +125,12 @@ def test_jit_concurrent_first_use(monkeypatch, tmp_path):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("spec", [(10, 3, [0o1157, 0o1753, 0o1331]), (10, 2, [0o1157, 0o1753]),
-                                  (9, 3, [0o557, 0o663, 0o711])], ids=["K10B3", "K10B2", "K9B3"])
+                                  (9, 3, [0o557, 0o663, 0o711]), (10, 4, [0o1157, 0o1753, 0o1331, 0o1475])],
+                         ids=["K10B3", "K10B2", "K9B3", "K10B4"])
 def test_metric_range_at_saturated_llrs(spec, monkeypatch, tmp_path):
     """The int16 metric range at its extreme: every LLR +-127 (random signs and
-    a long all-+127 run), K = 10 / 9 with B = 3 (the largest spread the fast
-    kernel admits), bit-exact vs the oracle."""
+    a long all-+127 run), K = 9 / 10 with B = 3 / 4 (the largest spreads the
+    fast kernel admits), bit-exact vs the oracle."""
     monkeypatch.setenv("VITDEC_JIT_CACHE", str(tmp_path))
     k, b, polys = spec
     rng = np.random.default_rng(k * 100 + b)

@@ -16,7 +16,7 @@ FMAH = {"VIADD.16x2", "IMAD", "IMAD.IADD", "IMAD.MOV.U32", "IMAD.X", "IMAD.SHL.U
 
 def main():
     obj = sys.argv[1] if len(sys.argv) > 1 else "paper_2011_09337_b200/build/vd_fast_k7.o"
-    pat = sys.argv[2] if len(sys.argv) > 2 else "CodeBILi7ELi2ELj121ELj91ELj0EEELi16ELb1ELb0ENS0_7NoPunct"
+    pat = sys.argv[2] if len(sys.argv) > 2 else "CodeBILi7ELi2ELj121ELj91ELj0ELj0EEELi16ELb1ELb0ENS0_7NoPunct"
     txt = subprocess.run(["cuobjdump", "-sass", obj], capture_output=True, text=True).stdout
     funcs = re.split(r"\n\s+Function : ", txt)
     f = next(x for x in funcs if pat in x.split("\n")[0])
