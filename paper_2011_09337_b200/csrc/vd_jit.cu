@@ -12,7 +12,8 @@
 //                         "" or "0": no disk cache)
 //
 // NVRTC is opened with dlopen on first use, so the library loads (and the
-// precompiled codes run) without it.
+// precompiled codes run) without it; codes that would need it then use the
+// generic kernel.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <sys/stat.h>
@@ -171,7 +172,9 @@ struct Entry {
 
 bool enabled() {
   const char* e = std::getenv("VITDEC_JIT");
-  return !(e && std::strcmp(e, "0") == 0);
+  if (e && std::strcmp(e, "0") == 0) return false;
+  // without NVRTC on this machine the codes keep the generic kernel
+  return nvrtc().ok;
 }
 
 const std::string& last_log() { return t_log; }
