@@ -176,14 +176,9 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
     return kHeader + static_cast<std::size_t>(fp.smem_per_warp) * c.w <= static_cast<std::size_t>(kSmemMax);
   };
   bool ok = false;
-  if (max_warps<C>() >= 16 && VD_GLOBAL_SPILL && warps_needed >= 16 * 148 && cap_rows < 0) {
-    // 16 warps per SM (4 per scheduler): TMEM + smem hold most rows, the rest
-    // spill to global scratch that stays L2-resident at this size
-    const Cand c16{16, 512};
-    ok = try_cand(c16, true);
-    if (ok) fp.warps_per_cta = 16;
-  }
-  if (!ok && ((VD_GLOBAL_SPILL == 2 && warps_needed >= 12 * 148) || cap_rows >= 0)) {
+  // Large launches: 12 warps per SM, TMEM + smem rows, and global rows for
+  // what does not fit (prefer the spill tier to fewer resident warps)
+  if (warps_needed >= 12 * 148 || cap_rows >= 0) {
     ok = try_cand(cands[0], true);
     fp.warps_per_cta = 12;
   }
@@ -196,7 +191,7 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
       ok = true;
     }
   }
-  if (!ok && VD_GLOBAL_SPILL) {
+  if (!ok) {
     // Long frames: 12 (or fewer for small launches) warps with TMEM + smem + global rows.
     for (const Cand& c : cands) {
       const bool last = &c == &cands[2];
@@ -246,7 +241,7 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream, KSel ksel
   // Head frames on the fast path via a zero-padded copy of the stream head
   // (exact, see FastParams::llr_head); otherwise they go to the generic kernel.
   const std::int64_t head_end = std::min<std::int64_t>((p.v1 + p.f - 1) / p.f, p.frame_end);
-  bool pad = VD_PAD_HEAD && p.nblocks == 0 && p.llr_stage0 == 0 && p.frame_begin < head_end &&
+  bool pad = p.nblocks == 0 && p.llr_stage0 == 0 && p.frame_begin < head_end &&
              plan<C, R>(p, &pl, true) && pl.fp.mi0 == p.frame_begin && pl.fp.mi1 >= head_end;
   if (!pad && !plan<C, R>(p, &pl)) return cudaErrorNotSupported;
   cudaError_t ek = cudaSuccess;

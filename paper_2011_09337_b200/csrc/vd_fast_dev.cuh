@@ -340,38 +340,20 @@ __device__ __forceinline__ std::uint32_t mad_u32(std::uint32_t a, std::uint32_t 
   return d;
 }
 
-// Compile-time tuning knobs (the defaults are the measured-best settings;
-// every rejected alternative is logged in profiles/r01_ab_notes.md /
-// profiles/r02_ab_notes.md and was removed from the source).
-#ifndef VD_NEG_FMA
-#define VD_NEG_FMA 1        // negated branch tables as IMAD (param-bank -1) on the FMA pipe (C5 +0.5 %, C4 +0.9 %)
-#endif
-#ifndef VD_FAST_TB
-#define VD_FAST_TB 1        // serial-traceback fast path (+6 %)
-#endif
-#ifndef VD_FAST_SUB_TB
-#define VD_FAST_SUB_TB 1    // subframe (stored-max parallel) traceback fast path
-#endif
-#ifndef VD_GLOBAL_SPILL
-#define VD_GLOBAL_SPILL 2   // 2 = prefer 12 warps + global rows; 1 = only when no on-chip layout fits; 0 = never
-#endif
-#ifndef VD_PAD_HEAD
-#define VD_PAD_HEAD 1       // head frames on the fast kernel via a zero-padded copy
-#endif
-#ifndef VD_TB_L2_PREFETCH
-#define VD_TB_L2_PREFETCH 1 // long-frame traceback: bulk L2 prefetch of the global rows ahead
-#endif
+// Tuning choices are the measured-best settings; every rejected alternative is
+// logged in profiles/r01_ab_notes.md / profiles/r02_ab_notes.md and was
+// removed from the source: negated branch tables as IMADs with a
+// parameter-bank -1 (C5 +0.5 %, C4 +0.9 %); the serial-traceback and
+// subframe-traceback fast paths (+6 %, +4-5 %); head frames through a
+// zero-padded copy; the long-frame traceback's bulk L2 prefetch.
 constexpr int kTbL2Rows = 64;  // rows (stages) per bulk L2 prefetch window
-#ifndef VD_MAX_WARPS
-#define VD_MAX_WARPS 12     // warps per CTA: 12 (16 = 4 per scheduler with L2-resident spill rows: C5 -5 %, C4 -4 %)
-#endif
-// Warps per CTA (launch bound). 16 = 4 per scheduler with part of the survivor
-// rows spilled to (L2-resident) global scratch was +3 % for K = 9 before the
-// block loop ran in mode runs; since then 12 is faster for every code
-// (C4 27.8 -> 29.0 Gbps, profiles/r01_ab_notes.md). 0 = per code (16 for K >= 9).
+// Warps per CTA (launch bound): 12 = 3 per scheduler, the most the TMEM +
+// shared-memory survivor store holds at f=256/20/20; 16 with part of the rows
+// spilled to (L2-resident) global scratch measured slower for every code
+// (C5 115 vs 123, C4 29.0 vs 29.9 Gbps, profiles/r02_ab_notes.md).
 template <class C>
 constexpr int max_warps() {
-  return VD_MAX_WARPS ? VD_MAX_WARPS : (C::kK >= 9 ? 16 : 12);
+  return 12;
 }
 
 // (a & m) | (b & ~m) as one LOP3 (m a compile-time constant after unrolling)
@@ -479,7 +461,7 @@ __device__ __forceinline__ void block_tables(const FrameState<GEO>& st, std::uin
 #pragma unroll
     for (int x = 0; x < GEO::NT; ++x) {
       // T[x ^ XM] = -T[x]
-      PT[k][x ^ XM] = VD_NEG_FMA ? mad_u32(PT[k][x], st.m1_p, OFFB) : OFFB - PT[k][x];
+      PT[k][x ^ XM] = mad_u32(PT[k][x], st.m1_p, OFFB);
     }
   }
 }
@@ -1116,7 +1098,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     // stage L-1 down to v1, output words aligned (f % 32 == 0). Per block:
     // one 4-word fetch, 4 x (funnel shift + bit select), 4 emitted bits into
     // a 32-bit accumulator stored with a plain 32-bit write every 8 blocks.
-    if (VD_FAST_TB && num_sub == 1 && ((L & (LB - 1)) == 0 || v2 >= LB) && (v1 & (LB - 1)) == 0 && (f & 31) == 0 &&
+    if (num_sub == 1 && ((L & (LB - 1)) == 0 || v2 >= LB) && (v1 & (LB - 1)) == 0 && (f & 31) == 0 &&
         __all_sync(kFull, ((obase + v1) & 31) == 0)) {
       std::uint32_t lp = P >> r;
       std::uint32_t u = (P & (R - 1)) | hsh;  // bit index into a decision word: register + 16 * half
@@ -1174,7 +1156,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         const std::uint32_t* grow = bc.grow_lane - lane + gcol;
         const unsigned char* grow_base = reinterpret_cast<const unsigned char*>(bc.grow_lane - lane);
         auto l2_prefetch = [&](int tb) {  // rows [tb - kTbL2Rows, tb) below the current block
-          if (VD_TB_L2_PREFETCH && lane == 0) {
+          if (lane == 0) {
             const int lo_row = max(tb - kTbL2Rows, t_gl) - t_gl, hi_row = tb - t_gl;
             if (hi_row > lo_row) {
               asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(grow_base + lo_row * 128),
@@ -1240,7 +1222,7 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     // f=320/20/45/32): every start stage has the same block phase, every
     // subframe emits whole aligned words; one uniform block loop over the
     // round, each lane walking only its own range (its top block partial).
-    if (VD_FAST_SUB_TB && num_sub > 1 && (step & 31) == 0 && (f % step) == 0 && (v1 & (LB - 1)) == 0 && v2 >= LB &&
+    if (num_sub > 1 && (step & 31) == 0 && (f % step) == 0 && (v1 & (LB - 1)) == 0 && v2 >= LB &&
         __all_sync(kFull, !active || ((obase + sub_lo) & 31) == 0)) {
       const int ph = (v1 + step + v2 - 1) & (LB - 1);  // phase of every start stage
       const int stb = st_t & ~(LB - 1);                // this lane's top block

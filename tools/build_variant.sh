@@ -1,7 +1,7 @@
 #!/bin/bash
 # Build a tuning variant of libvitdec_b200.so into build_variants/<name>/ with
 # extra nvcc flags (A/B kernel runs: VITDEC_LIB=build_variants/<name>/libvitdec_b200.so).
-#   tools/build_variant.sh w16 -DVD_MAX_WARPS=16   (run make first: vd_jit.cu includes build/vd_jit_sources.inc)
+#   tools/build_variant.sh myvariant -DSOME_MACRO=1   (run make first: vd_jit.cu includes build/vd_jit_sources.inc)
 set -e
 name=$1; shift
 ROOT=$(cd "$(dirname "$0")/.." && pwd)
