@@ -476,3 +476,39 @@ def test_small_launch_whole_words_over_stale_output(cfg, port):
     torch.cuda.synchronize()
     got = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
     assert np.array_equal(got, exp), np.flatnonzero(got != exp)[:10]
+
+
+@pytest.mark.parametrize("code", [K7, (7, 2, [0o133, 0o171]), (7, 3, [0o133, 0o171, 0o165]),
+                                  (9, 2, [0o561, 0o753]), (6, 2, [0o53, 0o75])],
+                         ids=["K7a", "K7b", "K7c", "K9a", "K6a"])
+def test_random_geometry_mid_sizes_vs_oracle(code, port):
+    """Random frame geometries (f, v1, v2, f0, traceback start) at sizes where
+    the fast kernels take the launch (small-launch kernel with its clipped tail
+    segments and whole-word output, or the 16-states-per-lane kernel with head
+    padding and generic edge frames), through the host streaming call and the
+    device call into a stale output buffer; bit-exact vs the oracle."""
+    import torch
+
+    from paper_2011_09337_b200.device import decode_i8_device
+
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng(9000 + k * 10 + b + polys[0])
+    for it in range(16):
+        n = int(rng.integers(20_000, 300_000))
+        f = int(rng.choice([32, 64, 96, 128, 200, 256, 320, 480, 512]))
+        f0 = int(rng.choice([0, 0, 32, f // 2 if f >= 64 else 0, int(rng.integers(1, f + 1))]))
+        cfg = vd.FrameConfig(f, int(rng.integers(0, 60)), int(rng.integers(0, 80)), f0,
+                             vd.TracebackStart(int(rng.integers(0, 2))), int(rng.integers(0, 2**63)))
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(0, 4)), int(rng.integers(0, 2**32)))
+        q = oracle.quantize(rx, [32.0, 4.0][it % 2])
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+        got = vd.unpack_bits(packed, n)
+        assert np.array_equal(got, exp), (code, n, cfg, np.flatnonzero(got != exp)[:8])
+        assert (stats.frames, stats.stages, stats.tracebacks) == st
+        out = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        decode_i8_device(t, cfg, n, torch.from_numpy(q).cuda(), 0, 0, -(-n // f), out, 0)
+        torch.cuda.synchronize()
+        got2 = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
+        assert np.array_equal(got2, exp), (code, n, cfg, "device", np.flatnonzero(got2 != exp)[:8])
