@@ -47,6 +47,8 @@ namespace jit {
 /// compile failure, see last_log()) on failure. VITDEC_JIT=0 disables it.
 bool enabled();
 const void* fast_kernel(int k, int b, const std::uint32_t* polys, bool tm, bool gl, cudaError_t* err);
+/// The small-launch kernel (vd_small_dev.cuh, 8 states per lane) for a rate-1/2 code.
+const void* small_kernel(int k, const std::uint32_t* polys, cudaError_t* err);
 const std::string& last_log();
 /// Compile only (no GPU needed): false + last_log() on failure.
 bool compile_check(int k, int b, const std::uint32_t* polys);

@@ -133,7 +133,7 @@ bool compile(const std::string& expr, std::string* cubin, std::string* name) {
     hdr_text.push_back(s.text);
     hdr_name.push_back(s.name);
   }
-  const std::string src = "#include \"vd_fast_dev.cuh\"\n";
+  const std::string src = "#include \"vd_fast_dev.cuh\"\n#include \"vd_small_dev.cuh\"\n";
   void* prog = nullptr;
   if (nv.create(&prog, src.c_str(), "vd_jit_fast.cu", static_cast<int>(hdr_text.size()), hdr_text.data(),
                 hdr_name.data()) != 0) {
@@ -179,12 +179,18 @@ bool enabled() {
 
 const std::string& last_log() { return t_log; }
 
-std::string expression(int k, int b, const std::uint32_t* polys, bool tm, bool gl) {
-  char buf[256];
-  std::snprintf(buf, sizeof(buf), "&vd::fast::fast_kernel<vd::fast::CodeB<%d, %d, %uu, %uu, %uu, %uu>, 16, %s, %s>", k,
-                b, polys[0], polys[1], b > 2 ? polys[2] : 0u, b > 3 ? polys[3] : 0u, tm ? "true" : "false",
-                gl ? "true" : "false");
+const void* kernel(const std::string& expr, cudaError_t* err);
+
+std::string code_type(int k, int b, const std::uint32_t* polys) {
+  char buf[160];
+  std::snprintf(buf, sizeof(buf), "vd::fast::CodeB<%d, %d, %uu, %uu, %uu, %uu>", k, b, polys[0], polys[1],
+                b > 2 ? polys[2] : 0u, b > 3 ? polys[3] : 0u);
   return buf;
+}
+
+std::string expression(int k, int b, const std::uint32_t* polys, bool tm, bool gl) {
+  return "&vd::fast::fast_kernel<" + code_type(k, b, polys) + ", 16, " + (tm ? "true" : "false") + ", " +
+         (gl ? "true" : "false") + ">";
 }
 
 bool compile_check(int k, int b, const std::uint32_t* polys) {
@@ -193,9 +199,16 @@ bool compile_check(int k, int b, const std::uint32_t* polys) {
 }
 
 const void* fast_kernel(int k, int b, const std::uint32_t* polys, bool tm, bool gl, cudaError_t* err) {
+  return kernel(expression(k, b, polys, tm, gl), err);
+}
+
+const void* small_kernel(int k, const std::uint32_t* polys, cudaError_t* err) {
+  return kernel("&vd::fast::small_kernel<" + code_type(k, 2, polys) + ", 8>", err);
+}
+
+const void* kernel(const std::string& expr, cudaError_t* err) {
   static std::mutex mu;
   static std::map<std::string, Entry> cache;
-  const std::string expr = expression(k, b, polys, tm, gl);
   std::lock_guard<std::mutex> lock(mu);
   auto it = cache.find(expr);
   if (it != cache.end()) return reinterpret_cast<const void*>(it->second.kern);

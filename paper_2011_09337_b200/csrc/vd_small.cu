@@ -38,7 +38,7 @@ bool plan_geom(const DecodeLaunch& p, std::int64_t mi0, std::int64_t mi1, int L,
   // survivor words: stages [SB floor(v1 / SB), SB nsb) + the traceback's over-read
   const int rows = (SG::SB * sp.nsb - SG::SB * (p.v1 / SG::SB)) / SG::SPW + 3;
   sp.llr_off = 0;
-  sp.dec_off = GEO::FPW * sp.pitch;
+  sp.dec_off = (GEO::FPW * sp.pitch + 15) & ~15;  // (16-byte rows below: the relayout's LDS.128)
   sp.x_off = sp.dec_off + rows * 32 * 4;
   sp.ss_off = sp.x_off + GEO::GROUPS * GEO::XSTRIDE * 4;
   sp.smem_per_warp = (sp.ss_off + GEO::FPW * sp.num_sub * 2 + 15) & ~15;
@@ -99,18 +99,53 @@ bool plan_small(const DecodeLaunch& p, SmallLaunch* out) {
   return true;
 }
 
-template <class C, int R>
-cudaError_t launch_small(const SmallLaunch& sl, cudaStream_t stream) {
+cudaError_t launch_kernel(const void* kern, const SmallLaunch& sl, cudaStream_t stream) {
   const std::int64_t warps = sl.warp_begin[sl.nseg];
   const std::int64_t blocks = (warps + sl.warps_per_cta - 1) / sl.warps_per_cta;
   const std::size_t smem = static_cast<std::size_t>(sl.smem_per_warp) * sl.warps_per_cta;
-  // (always the maximum: host threads launching different geometries at once
-  // must not lower the limit under each other's launches)
-  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(small_kernel<C, R>));
+  cudaError_t e = allow_max_smem(kern);
   if (e != cudaSuccess) return e;
-  small_kernel<C, R><<<static_cast<unsigned>(blocks), sl.warps_per_cta * 32, smem, stream>>>(sl);
+  SmallLaunch arg = sl;
+  void* args[] = {&arg};
+  e = cudaLaunchKernel(kern, dim3(static_cast<unsigned>(blocks)), dim3(sl.warps_per_cta * 32), args, smem, stream);
   note_launch();
-  return cudaGetLastError();
+  return e;
+}
+
+template <class C, int R>
+cudaError_t launch_small(const SmallLaunch& sl, cudaStream_t stream) {
+  return launch_kernel(reinterpret_cast<const void*>(small_kernel<C, R>), sl, stream);
+}
+
+// Placeholder code of a K class for planning (plan_small uses only K and B);
+// the kernel of any other rate-1/2 code comes from the run-time instantiation.
+template <int K>
+using SmallPlanCode = CodeB<K, 2, (1u << (K - 1)) | 1u, (1u << (K - 1)) | 1u>;
+
+template <int K>
+bool try_jit_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe, bool* whole) {
+  SmallLaunch sl;
+  if (!plan_small<SmallPlanCode<K>, 8>(p, &sl)) return false;
+  if (whole) *whole = sl.whole_words;
+  if (probe) return true;
+  cudaError_t ek = cudaSuccess;
+  const void* kern = jit::small_kernel(p.k, p.polys, &ek);
+  *err = kern ? launch_kernel(kern, sl, stream) : (ek != cudaSuccess ? ek : cudaErrorInvalidSource);
+  return true;
+}
+
+bool jit_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, bool probe, bool* whole) {
+  if (p.b != 2 || !jit::enabled()) return false;
+  switch (p.k) {
+    case 5: return try_jit_small<5>(p, stream, err, probe, whole);
+    case 6: return try_jit_small<6>(p, stream, err, probe, whole);
+    case 7: return try_jit_small<7>(p, stream, err, probe, whole);
+    // K = 8 / 9 instantiate and decode correctly, but lose to the
+    // 16-states-per-lane kernel at every small-launch size measured (C1:
+    // 13.1 vs 19.7 Gbps at K = 8, 9.3 vs 10.8 at K = 9; profiles/r02_ab_notes.md):
+    // twice the warps and a 16 / 32-lane relayout per 3 stages. They stay on it.
+    default: return false;
+  }
 }
 
 }  // namespace
@@ -140,16 +175,22 @@ bool plan_any(const DecodeLaunch& p, SmallLaunch* sl, int* code) {
 bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
   SmallLaunch sl;
   int code = -1;
-  if (!plan_any(p, &sl, &code)) return false;
-  *err = code == 0 ? launch_small<K7a, 8>(sl, stream) : launch_small<K7b, 8>(sl, stream);
-  return true;
+  if (plan_any(p, &sl, &code)) {
+    *err = code == 0 ? launch_small<K7a, 8>(sl, stream) : launch_small<K7b, 8>(sl, stream);
+    return true;
+  }
+  if (K7a::matches(p.k, p.b, p.polys) || K7b::matches(p.k, p.b, p.polys)) return false;
+  return jit_small(p, stream, err, false, nullptr);
 }
 
 bool small_writes_whole_words(const DecodeLaunch& p) {
   if (!small_launch_wanted(p)) return false;
   SmallLaunch sl;
   int code = -1;
-  return plan_any(p, &sl, &code) && sl.whole_words;
+  if (plan_any(p, &sl, &code)) return sl.whole_words;
+  if (K7a::matches(p.k, p.b, p.polys) || K7b::matches(p.k, p.b, p.polys)) return false;
+  bool whole = false;
+  return jit_small(p, nullptr, nullptr, true, &whole) && whole;
 }
 
 }  // namespace fast

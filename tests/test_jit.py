@@ -145,3 +145,42 @@ def test_metric_range_at_saturated_llrs(spec, monkeypatch, tmp_path):
         packed, stats = vd.framed_decode_stream(q, n, t, cfg)
         got = vd.unpack_bits(packed, n)
         assert np.array_equal(got, exp), (spec, cfg, np.flatnonzero(got != exp)[:10])
+
+
+SMALL_JIT_CODES = [
+    (9, 2, [0o561, 0o753]),         # K = 8 / 9: the 16-states-per-lane kernel either way
+    (8, 2, [0o247, 0o170]),         # not paired
+    (6, 2, [0o65, 0o57]),
+    (5, 2, [0o22, 0o35]),           # not paired
+    (7, 2, [0o165, 0o117]),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("spec", SMALL_JIT_CODES, ids=lambda s: f"K{s[0]}_{s[2][0]:o}")
+def test_jit_small_launch_vs_oracle(spec, monkeypatch, tmp_path):
+    """Small launches of rate-1/2 codes with K <= 7 other than the two
+    precompiled K = 7 ones run a run-time instantiation of the 8-states-per-lane kernel
+    (csrc/vd_small_dev.cuh): bit-exact vs the oracle and vs the
+    16-states-per-lane kernel (VITDEC_SMALL=0), over subframe, random-start,
+    head-padded and clipped-tail geometries."""
+    monkeypatch.setenv("VITDEC_JIT_CACHE", str(tmp_path))
+    k, b, polys = spec
+    port = oracle.port()
+    t = trellis(spec)
+    rng = np.random.default_rng(9100 + k * 10 + polys[0])
+    cfgs = [vd.FrameConfig(256, 20, 20), vd.FrameConfig(320, 20, 45, 32),
+            vd.FrameConfig(128, 20, 40, 32, vd.TracebackStart.kRandom, 5), vd.FrameConfig(100, 14, 30, 30),
+            vd.FrameConfig(96, 7, 11, 0)]
+    for i, cfg in enumerate(cfgs):
+        n = int(rng.integers(40_000, 200_000))
+        rx, _ = port.gen_bench_block(k, b, polys, n, float(rng.uniform(0, 4)), 700 + i)
+        q = oracle.quantize(rx, [32.0, 4.0][i % 2])
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0, int(cfg.start), cfg.seed)
+        for small in ("1", "0"):
+            monkeypatch.setenv("VITDEC_SMALL", small)
+            packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+            got = vd.unpack_bits(packed, n)
+            bad = np.flatnonzero(got != exp)
+            assert bad.size == 0, (spec, small, cfg, n, bad[:10], bad.size)
+            assert (stats.frames, stats.stages, stats.tracebacks) == st
