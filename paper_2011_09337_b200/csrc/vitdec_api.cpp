@@ -4,6 +4,7 @@
 // GPU, everything else keeps the reference's semantics and exception
 // messages.
 #include <algorithm>
+#include <array>
 #include <atomic>
 #include <cmath>
 #include <cstdlib>
@@ -15,6 +16,10 @@
 #include <vector>
 
 #include <cuda_runtime.h>
+#include <sys/mman.h>
+#if defined(__SSE2__)
+#include <emmintrin.h>
+#endif
 
 #include "vitdec/decoder.hpp"
 #include "vitdec/trellis.hpp"
@@ -22,6 +27,12 @@
 
 namespace vitdec {
 namespace {
+
+#ifdef MADV_POPULATE_WRITE
+constexpr int kMadvPopulateWrite = MADV_POPULATE_WRITE;
+#else
+constexpr int kMadvPopulateWrite = 23;  // Linux >= 5.14
+#endif
 
 [[noreturn]] void raise(vd_status st) {
   const std::string msg = vd_last_error();
@@ -67,9 +78,6 @@ int env_gpus() {
   return g > 0 ? g : 0;
 }
 
-// True when every value is an integer in [-127, 127]: the block is then
-// decoded by the int8 fixed-point kernels, exactly (integer sums are exact in
-// both the reference's double arithmetic and the kernel's int32 arithmetic).
 // Runs fn(lo, hi) over [0, n) on `workers` host threads (the reference's
 // `workers` argument, parallel.hpp:11-29 semantics: contiguous chunks, joined
 // before return); small ranges stay on the calling thread.
@@ -130,33 +138,112 @@ struct HostScratch {
 };
 thread_local HostScratch t_scratch;
 
-// Integer-valued blocks in [-127, 127] decode exactly on the int8 kernels.
+// One value: clamp (NaN -> -127), truncate; v is an integer in [-127, 127]
+// iff the truncated value equals it.
+inline int int8_one(double v, std::int8_t* out) {
+  const int iv = static_cast<int>(std::fmin(std::fmax(v, -127.0), 127.0));
+  *out = static_cast<std::int8_t>(iv);
+  return static_cast<double>(iv) != v;
+}
+
+// Range [lo, hi) of int8_exact; nonzero if a value is not an int8 integer.
+// SSE2 (every x86-64): 16 doubles per iteration, clamp by MINPD / MAXPD (a
+// NaN clamps to 127 and then fails the equality test), CVTTPD2DQ, the
+// round-trip compare, and saturating packs (exact: the values are already in
+// [-127, 127]). The scalar libm fmin / fmax loop ran at ~6 ns per value.
+int int8_range(const double* d, std::int8_t* out, std::int64_t lo, std::int64_t hi) {
+  int bad = 0;
+  std::int64_t i = lo;
+#if defined(__SSE2__)
+  const __m128d cmin = _mm_set1_pd(-127.0), cmax = _mm_set1_pd(127.0);
+  __m128d badv = _mm_setzero_pd();
+  for (; i + 16 <= hi; i += 16) {
+    __m128i w[4];
+    for (int k = 0; k < 4; ++k) {
+      const __m128d v0 = _mm_loadu_pd(d + i + 4 * k), v1 = _mm_loadu_pd(d + i + 4 * k + 2);
+      const __m128i i0 = _mm_cvttpd_epi32(_mm_max_pd(_mm_min_pd(v0, cmax), cmin));
+      const __m128i i1 = _mm_cvttpd_epi32(_mm_max_pd(_mm_min_pd(v1, cmax), cmin));
+      badv = _mm_or_pd(badv, _mm_cmpneq_pd(_mm_cvtepi32_pd(i0), v0));
+      badv = _mm_or_pd(badv, _mm_cmpneq_pd(_mm_cvtepi32_pd(i1), v1));
+      w[k] = _mm_unpacklo_epi64(i0, i1);
+    }
+    const __m128i b = _mm_packs_epi16(_mm_packs_epi32(w[0], w[1]), _mm_packs_epi32(w[2], w[3]));
+    _mm_storeu_si128(reinterpret_cast<__m128i*>(out + i), b);
+  }
+  bad |= _mm_movemask_pd(badv);
+#endif
+  for (; i < hi; ++i) bad |= int8_one(d[i], out + i);
+  return bad;
+}
+
+// True when every value is an integer in [-127, 127]: the block is then
+// decoded by the int8 fixed-point kernels, exactly (integer sums are exact in
+// both the reference's double arithmetic and the kernel's int32 arithmetic).
 bool int8_exact(const LlrBlock& llr, std::int8_t* out, int workers) {
-  const Eigen::Index n = llr.size();
   const double* d = llr.data();
   std::atomic<bool> ok{true};
-  host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
-    int bad = 0;
-    for (std::int64_t i = lo; i < hi; ++i) {  // branch-free, no libm rounding call
-      const double v = d[i];
-      // clamp (NaN -> -127), truncate: v is an integer in [-127, 127] iff the
-      // truncated value equals it
-      const int iv = static_cast<int>(std::fmin(std::fmax(v, -127.0), 127.0));
-      bad |= static_cast<double>(iv) != v;
-      out[i] = static_cast<std::int8_t>(iv);
-    }
-    if (bad) ok.store(false, std::memory_order_relaxed);
+  host_parallel(llr.size(), workers, [&](std::int64_t lo, std::int64_t hi) {
+    if (int8_range(d, out, lo, hi)) ok.store(false, std::memory_order_relaxed);
   });
   return ok.load();
 }
 
-BitVec unpack(const std::uint32_t* packed, Eigen::Index n, int workers = 1) {
-  BitVec bits(static_cast<std::size_t>(n));
-  host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
-    for (std::int64_t i = lo; i < hi; ++i) bits[i] = static_cast<std::uint8_t>((packed[i >> 5] >> (i & 31)) & 1u);
-  });
+// A BitVec of n bytes whose pages are already faulted in. A fresh multi-MiB
+// vector is an mmap, and first-touch faults in the single-threaded zero-fill
+// of std::vector's constructor cost more than the decode (2^26 bits: 23 ms);
+// `workers` threads fault their own ranges in first (MADV_POPULATE_WRITE).
+BitVec resident_bits(Eigen::Index n, int workers) {
+  BitVec bits;
+  bits.reserve(static_cast<std::size_t>(n));
+  constexpr std::uintptr_t kPage = 4096;
+  if (n >= (std::int64_t{4} << 20)) {
+    const auto base = reinterpret_cast<std::uintptr_t>(bits.data());
+    host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
+      const std::uintptr_t a = (base + lo + kPage - 1) & ~(kPage - 1), b = (base + hi) & ~(kPage - 1);
+      if (b > a) madvise(reinterpret_cast<void*>(a), b - a, kMadvPopulateWrite);  // (advisory: failure is harmless)
+    });
+  }
+  bits.resize(static_cast<std::size_t>(n));
   return bits;
 }
+
+// One byte per bit from the packed words, 8 bytes per table lookup.
+void unpack_into(BitVec& bits, const std::uint32_t* packed, Eigen::Index n, int workers = 1) {
+  static const auto lut = [] {
+    std::array<std::uint64_t, 256> t{};
+    for (int v = 0; v < 256; ++v)
+      for (int j = 0; j < 8; ++j) t[v] |= static_cast<std::uint64_t>((v >> j) & 1) << (8 * j);
+    return t;
+  }();
+  std::uint8_t* out = bits.data();
+  const std::int64_t nbytes = n / 8;  // whole packed bytes
+  const auto* pb = reinterpret_cast<const std::uint8_t*>(packed);  // (little-endian: bit i is bit i % 8 of byte i / 8)
+  host_parallel(nbytes, workers, [&](std::int64_t lo, std::int64_t hi) {
+    for (std::int64_t j = lo; j < hi; ++j) std::memcpy(out + 8 * j, &lut[pb[j]], 8);
+  });
+  for (std::int64_t i = 8 * nbytes; i < n; ++i) out[i] = static_cast<std::uint8_t>((packed[i >> 5] >> (i & 31)) & 1u);
+}
+
+BitVec unpack(const std::uint32_t* packed, Eigen::Index n) {
+  BitVec bits(static_cast<std::size_t>(n));
+  unpack_into(bits, packed, n);
+  return bits;
+}
+
+// Runs fn on its own thread from construction; joined by wait() or the
+// destructor (also on an exception unwinding the caller).
+class Background {
+ public:
+  template <typename Fn>
+  explicit Background(Fn&& fn) : th_(std::forward<Fn>(fn)) {}
+  ~Background() { wait(); }
+  void wait() {
+    if (th_.joinable()) th_.join();
+  }
+
+ private:
+  std::thread th_;
+};
 
 }  // namespace
 
@@ -283,14 +370,17 @@ DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const Fr
   vd_exec ex{};
   ex.num_devices = env_gpus();
   auto* q = static_cast<std::int8_t*>(t_scratch.get(0, static_cast<std::size_t>(llr.size())));
+  // the returned bits' pages are faulted in beside the conversion and decode
+  DecodeOutput out;
+  Background prep([&out, n, workers] { out.bits = resident_bits(n, std::max(1, workers / 4)); });
   // `workers` host threads prepare the block / unpack the bits (the GPU does the decode)
   if (int8_exact(llr, q, workers)) {
     check(vd_decode_i8(trellis.native(), &c, q, n, packed, &st, &ex));
   } else {
     check(vd_decode_f64(trellis.native(), &c, llr.data(), n, packed, &st, &ex));
   }
-  DecodeOutput out;
-  out.bits = unpack(packed, n, workers);
+  prep.wait();
+  unpack_into(out.bits, packed, n, workers);
   out.stats = from_c(st);
   return out;
 }
