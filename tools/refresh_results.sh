@@ -22,6 +22,10 @@ b() {  # bench.py line -> {"row", "gbps", "frac", "ber"}
   b "C5 f=512/20/63 2^28" --frame 512,20,63 --stages 268435456
   b "C5 f=1024/42/42 2^28" --frame 1024,42,42 --stages 268435456
   b "C5 JIT code (165,117) 2^30" --stages 1073741824 --polys 165,117
+  b "C1 JIT code (165,117)" --workload C1 --polys 165,117
+  b "C1 K=6 (65,57) JIT" --workload C1 --k 6 --polys 65,57
+  b "K=9 r1/4 (765,671,513,473) 2^28" --workload C4 --polys 765,671,513,473
+  b "K=10 (1157,1753) 2^28" --workload C4 --k 10 --polys 1157,1753
 } > $out/${tag}_workloads.jsonl
 bash tools/sweep_frames.sh > $out/${tag}_frame_sweep.jsonl 2>&1
 timeout 600 python tools/bench_batch.py > $out/${tag}_batch.jsonl 2>&1
