@@ -1396,16 +1396,16 @@ vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg*
   DeviceGuard guard(dev);
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const std::int64_t nf = num_frames(cfg, n);
-  // Fused depuncture (vd_fast.cuh Punct, VITDEC_PUNCT_FUSED=1): the fast
-  // kernel stages the punctured stream straight into its shared-memory LLR
-  // ring; the few edge frames it does not take are decoded from dense copies
-  // of their windows. Off by default: measured against the separate
-  // HBM-streaming depuncture pass on one B200 (2^30 stages, f=240/24/24) it
-  // ran at 0.99x (r2/3) and 0.54x (r3/4) of pass + decode
+  // Fused depuncture (vd_fast_dev.cuh Punct; the default, VITDEC_PUNCT_FUSED=0
+  // turns it off): the fast kernel stages the punctured stream straight into
+  // its shared-memory LLR ring; the few edge frames it does not take are
+  // decoded from dense copies of their windows on the side stream. Measured
+  // against the separate HBM-streaming depuncture pass + decode on one B200
+  // (2^30 stages, f=240/24/24): 1.05x (r2/3), 1.04x (r3/4)
   // (profiles/r02_puncture_bench.jsonl, profiles/r02_ab_notes.md).
   const int pid = punct_pattern_id(pp);
   const char* env_fused = std::getenv("VITDEC_PUNCT_FUSED");
-  const bool want_fused = pid != 0 && env_fused && std::atoi(env_fused) != 0 &&
+  const bool want_fused = pid != 0 && !(env_fused && std::atoi(env_fused) == 0) &&
                           (reinterpret_cast<std::uintptr_t>(punctured_dev) & 3u) == 0 && cfg->f0 == 0;
   if (want_fused && check_gpu_envelope(code) == VD_OK) {
     vd::DecodeLaunch p;
@@ -1431,31 +1431,40 @@ vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg*
       const std::uint32_t* in_out = nullptr;
       if (vd_status st = device_table(code, dev, &in_out)) return st;
       p.in_out = in_out;
-      // edge frames first (their zeroing of shared output words must precede
-      // the fused kernel's writes), each from a dense copy of its window
+      // Every output word is zeroed first (all kernels OR their bits in;
+      // edge and interior frames share at most the two boundary words), then
+      // the edge frames — each decoded from a dense depunctured copy of its
+      // window — run on the side stream beside the fused kernel.
+      VD_CUDA(cudaMemsetAsync(out_dev, 0, sizeof(std::uint32_t) * static_cast<std::size_t>((n + 31) / 32), s),
+              "zero output");
+      const bool edges = mi0 > 0 || mi1 < nf;
+      cudaStream_t side = nullptr;
+      if (edges) VD_CUDA(vd::side_fork(s, &side), "side stream");
+      auto decode_edge = [&](std::int64_t llr_stage0, std::int64_t fb, std::int64_t fe, std::int64_t out_stage0) {
+        vd::DecodeLaunch e = p;
+        e.llr = llr_scratch_dev;
+        e.llr_stage0 = llr_stage0;
+        e.frame_begin = fb;
+        e.frame_end = fe;
+        e.out = out_dev + out_stage0 / 32;
+        e.out_stage0 = out_stage0;
+        return vd::fast_path_supported(e) ? vd::launch_fast_i8(e, side) : vd::launch_generic_i8(e, side);
+      };
       if (mi0 > 0) {
         const std::int64_t t1 = std::min<std::int64_t>(mi0 * cfg->f + cfg->v2 + vd::kPfSlackStages, n);
-        if (vd_status st = launch_depuncture(pp, punctured_dev, 0, t1, llr_scratch_dev, s)) return st;
-        if (vd_status st = decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, 0, 0, mi0, out_dev, 0, nullptr,
-                                                      dev, stream))
-          return st;
+        if (vd_status st = launch_depuncture(pp, punctured_dev, 0, t1, llr_scratch_dev, side)) return st;
+        VD_CUDA(decode_edge(0, 0, mi0, 0), "edge frames");
       }
       if (mi1 < nf) {
         const std::int64_t t0 = mi1 * cfg->f - cfg->v1;  // a period multiple: f and v1 are
-        if (vd_status st = launch_depuncture(pp, punctured_dev + pp.off(t0), t0, n - t0, llr_scratch_dev, s))
+        if (vd_status st = launch_depuncture(pp, punctured_dev + pp.off(t0), t0, n - t0, llr_scratch_dev, side))
           return st;
-        const std::int64_t ow = (mi1 * cfg->f) / 32 * 32;
-        if (vd_status st = decode_device<std::int8_t>(code, cfg, n, llr_scratch_dev, t0, mi1, nf, out_dev + ow / 32, ow,
-                                                      nullptr, dev, stream))
-          return st;
+        VD_CUDA(decode_edge(t0, mi1, nf, (mi1 * cfg->f) / 32 * 32), "edge frames");
       }
-      // interior frames: zero their own words (minus the edge-shared ones), then the fused kernel
-      const std::int64_t w0 = (mi0 * cfg->f + 31) / 32;
-      const std::int64_t w1 = mi1 < nf ? (mi1 * cfg->f) / 32 : (n + 31) / 32;
-      if (w1 > w0) VD_CUDA(cudaMemsetAsync(out_dev + w0, 0, sizeof(std::uint32_t) * (w1 - w0), s), "zero output");
       cudaError_t e = cudaSuccess;
       if (!vd::launch_fast_punct_i8(p, pid, s, &e, &mi0, &mi1)) return fail(VD_ECUDA, "fused depuncture plan changed");
       if (e != cudaSuccess) return cuda_fail(e, "fused depuncture decode");
+      if (edges) VD_CUDA(vd::side_join(s), "side stream");
       return VD_OK;
     }
   }

@@ -119,6 +119,22 @@ bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t strea
   return fast::try_punct_k7(p, pattern, stream, err, mi0, mi1);
 }
 
+cudaError_t side_fork(cudaStream_t main, cudaStream_t* side) {
+  fast::SideStream* ss = fast::side_stream();
+  if (!ss) return cudaErrorUnknown;
+  if (cudaError_t e = cudaEventRecord(ss->fork, main); e != cudaSuccess) return e;
+  if (cudaError_t e = cudaStreamWaitEvent(ss->s, ss->fork, 0); e != cudaSuccess) return e;
+  *side = ss->s;
+  return cudaSuccess;
+}
+
+cudaError_t side_join(cudaStream_t main) {
+  fast::SideStream* ss = fast::side_stream();
+  if (!ss) return cudaErrorUnknown;
+  if (cudaError_t e = cudaEventRecord(ss->join, ss->s); e != cudaSuccess) return e;
+  return cudaStreamWaitEvent(main, ss->join, 0);
+}
+
 bool fast_output_whole_words(const DecodeLaunch& p) {
   return fast_path_supported(p) && fast::small_writes_whole_words(p);
 }

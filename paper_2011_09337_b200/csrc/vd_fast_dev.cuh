@@ -128,6 +128,22 @@ struct Punct {
     for (int j = 0; j < 4; ++j) m |= (src(i, j) >= 0 ? 0xffu : 0u) << (8 * j);
     return m;
   }
+  /// The gather of one fill task's 6 output words as one constant-evaluated
+  /// table (called from device code, the functions above were left to run
+  /// time for P = 3: ~360 uniform-datapath instructions per block).
+  struct Gather {
+    int word[6];
+    std::uint32_t sel[6], mask[6];
+  };
+  static constexpr Gather gather() {
+    Gather g{};
+    for (int i = 0; i < 6; ++i) {
+      g.word[i] = lo_src(i) / 4;
+      g.sel[i] = sel(i);
+      g.mask[i] = mask(i);
+    }
+    return g;
+  }
 };
 struct NoPunct {
   static constexpr bool kActive = false;
@@ -752,11 +768,12 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
       std::uint32_t u[5];
 #pragma unroll
       for (int j = 0; j < 5; ++j) u[j] = __funnelshift_r(raw[j], raw[j + 1], 8u * ralign);
+      constexpr typename PN::Gather G = PN::gather();
       std::uint32_t o[6];
 #pragma unroll
       for (int i = 0; i < 6; ++i) {
-        const int a = PN::lo_src(i) / 4;
-        o[i] = prmt(u[a], u[a + 1 < 5 ? a + 1 : 4], PN::sel(i)) & PN::mask(i);
+        const int a = G.word[i];
+        o[i] = prmt(u[a], u[a + 1 < 5 ? a + 1 : 4], G.sel[i]) & G.mask[i];
       }
       if (tvalid) {
         const std::uint32_t s = stg_s + ((c & 1) ? kChunkBytes : 0u) + static_cast<std::uint32_t>(lane >> 1) * 48u +
@@ -986,9 +1003,18 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
     if constexpr (PN::kActive) {
       const std::uint32_t sA = stg_s + rbuf + static_cast<std::uint32_t>(2 * grp) * 48u + static_cast<std::uint32_t>(rpos) * 8u;
       run_block<C, GEO, MD, TM, GL, BUF, PN>(st, blk, bc, tprev, pfA, pfB, sA, rec);
-      if (rc + 1 < nch) {
-        if (rpos == 2) fill_issue(rc + 1);
-        if (rpos == 4) fill_finish(rc + 1);
+      // (rpos = (blk + 2) % 6 has the parity of blk: the fills only ever
+      // fall on the first block of a pair, and as branches, not predicated
+      // every block — ptxas if-converted them for P = 3: +24 issued
+      // instructions per block)
+      if constexpr (BUF == 0) {
+        if (rc + 1 < nch) {
+          if (__builtin_expect(rpos == 2, 0)) {
+            fill_issue(rc + 1);
+          } else if (__builtin_expect(rpos == 4, 0)) {
+            fill_finish(rc + 1);
+          }
+        }
       }
       if (++rpos == 6) {
         rpos = 0;

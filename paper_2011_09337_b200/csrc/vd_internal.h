@@ -41,6 +41,13 @@ bool fast_output_whole_words(const DecodeLaunch& p);
 /// and err == nullptr: plan only). False: not supported for this code/config.
 bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err,
                           std::int64_t* mi0, std::int64_t* mi1);
+/// The calling thread's side stream on the current device (the one the fast
+/// launches use for edge frames): side_fork makes it wait for the work
+/// enqueued on `main` so far and returns it; side_join makes `main` wait for
+/// the work enqueued on it so far. (Launches on the side stream may use it
+/// themselves: the waits are captured at enqueue time.)
+cudaError_t side_fork(cudaStream_t main, cudaStream_t* side);
+cudaError_t side_join(cudaStream_t main);
 namespace jit {
 /// Run-time (NVRTC) instantiation of the fast kernel for a code outside the
 /// precompiled list (vd_jit.cu); nullptr + *err (cudaErrorInvalidSource:

@@ -98,10 +98,10 @@ def main():
         ok_dep = bool(np.array_equal(scratch[: want.size].cpu().numpy(), want))
         import os
 
-        os.environ["VITDEC_PUNCT_FUSED"] = "0"  # A/B: separate depuncture pass + decode (default)
+        os.environ["VITDEC_PUNCT_FUSED"] = "0"  # A/B: separate depuncture pass + decode
         dec_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
         sep_out = out.clone()
-        os.environ["VITDEC_PUNCT_FUSED"] = "1"  # depuncture fused into the fast kernel's LLR staging (opt-in)
+        os.environ["VITDEC_PUNCT_FUSED"] = "1"  # depuncture fused into the fast kernel's LLR staging (default)
         fused_s = timed(lambda: decode_punctured_i8_device(t, cfg, p, punct, punct_h.size, scratch, out, -1, s))
         fused_same = bool(torch.equal(out[: n // 32], sep_out[: n // 32]))
         os.environ.pop("VITDEC_PUNCT_FUSED")
