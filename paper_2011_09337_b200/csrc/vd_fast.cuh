@@ -74,6 +74,12 @@ inline SideStream* side_stream() {
   return &(cache.m[dev] = ss);
 }
 
+// Small-launch kernel (vd_small.cu): a single-round launch's edge frames, and
+// the partial last round of a multi-round launch.
+bool small_launch_wanted(const DecodeLaunch& p);
+bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err);
+bool small_can_take(const DecodeLaunch& p);  // plan only: one round of the small kernel
+
 struct Plan {
   FastParams fp;
   std::size_t smem;
@@ -182,10 +188,14 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
     ok = try_cand(cands[0], true);
     fp.warps_per_cta = 12;
   }
-  for (const Cand& c : cands) {
-    if (ok) break;
-    const bool last = &c == &cands[2];
-    if (!last && warps_needed < static_cast<std::int64_t>(c.w) * 148) continue;  // would not fill the GPU
+  // Smaller launches: the fewest warps per CTA that still hold every frame
+  // group in one round (the runtime keeps one TMEM kernel CTA per SM:
+  // cudaOccupancyMaxActiveBlocksPerMultiprocessor = 1 even for 4-warp CTAs),
+  // which also leaves shared memory beside it for the edge frames' launch.
+  const std::int64_t sms = sm_count();
+  for (int i = 2; i >= 0 && !ok; --i) {  // 4, 8, 12 warps
+    const Cand& c = cands[i];
+    if (i > 0 && warps_needed > static_cast<std::int64_t>(c.w) * sms) continue;  // would need more rounds
     if (try_cand(c, false)) {
       fp.warps_per_cta = c.w;
       ok = true;
@@ -193,13 +203,12 @@ bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   }
   if (!ok) {
     // Long frames: 12 (or fewer for small launches) warps with TMEM + smem + global rows.
-    for (const Cand& c : cands) {
-      const bool last = &c == &cands[2];
-      if (!last && warps_needed < static_cast<std::int64_t>(c.w) * 148) continue;
+    for (int i = 2; i >= 0 && !ok; --i) {
+      const Cand& c = cands[i];
+      if (i > 0 && warps_needed > static_cast<std::int64_t>(c.w) * sms) continue;
       if (try_cand(c, true)) {
         fp.warps_per_cta = c.w;
         ok = true;
-        break;
       }
     }
   }
@@ -265,37 +274,12 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream, KSel ksel
     pl.fp.llr_head = head_buf;
   }
   const FastParams& fp = pl.fp;
-  // Edge frames (clipped windows) go to the generic kernel on a side stream,
-  // concurrently with the fast kernel (they fit beside its CTA on an SM).
-  const bool edges = p.nblocks == 0 && (fp.mi0 > p.frame_begin || fp.mi1 < p.frame_end);
-  SideStream* side = nullptr;
-  if (edges) {
-    side = side_stream();
-    if (!side) return cudaErrorUnknown;
-    if (cudaError_t err = cudaEventRecord(side->fork, stream); err != cudaSuccess) return err;
-    if (cudaError_t err = cudaStreamWaitEvent(side->s, side->fork, 0); err != cudaSuccess) return err;
-  }
-  if (edges && fp.mi0 > p.frame_begin) {
-    DecodeLaunch e = p;
-    e.frame_end = fp.mi0;
-    if (cudaError_t err = launch_generic_i8(e, side->s); err != cudaSuccess) return err;
-  }
-  if (edges && fp.mi1 < p.frame_end) {
-    DecodeLaunch e = p;
-    e.frame_begin = fp.mi1;
-    if (p.sigma) e.sigma = static_cast<std::int64_t*>(p.sigma) + (fp.mi1 - p.frame_begin) * p.s;
-    if (cudaError_t err = launch_generic_i8(e, side->s); err != cudaSuccess) return err;
-  }
-  if (edges) {
-    if (cudaError_t err = cudaEventRecord(side->join, side->s); err != cudaSuccess) return err;
-  }
   const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
   std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
   // (always the maximum: host threads launching different plans at once must
   // not lower the limit under each other's launches)
   cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
   if (e != cudaSuccess) return e;
-  FastParams fpl = fp;
   // persistent grid: as many CTAs as are co-resident (one per SM with TMEM)
   int per_sm = 1;
   if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, fp.warps_per_cta * 32, pl.smem) != cudaSuccess ||
@@ -303,7 +287,60 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream, KSel ksel
     cudaGetLastError();
     per_sm = 1;
   }
-  blocks = std::min<std::int64_t>(blocks, static_cast<std::int64_t>(sm_count()) * per_sm);
+  const std::int64_t resident = static_cast<std::int64_t>(sm_count()) * per_sm;
+  // Edge frames (clipped windows) run on a side stream, concurrently with the
+  // fast kernel. Generic kernel (one warp per frame, fits beside the fast
+  // kernel's CTAs; ~100 us for a 296-stage window) by default; when the fast
+  // launch is a single round of partly filled CTAs (mid-size decodes, where
+  // that latency would be the critical path) the small-launch kernel (~30 us)
+  // takes them instead, beside it.
+  // Multi-round launches whose last round would hold only a few frame groups
+  // (on a few SMs, at the full per-round time): those groups and the tail
+  // edge frames go to one small-kernel launch after the fast kernel instead
+  // (2^23 stages: 2048 groups = 1776 + 272, see profiles/r02_ab_notes.md).
+  std::int64_t mi1_fast = fp.mi1;
+  DecodeLaunch rest = p;
+  bool small_rest = false;
+  if (p.nblocks == 0 && blocks > resident) {
+    const std::int64_t slots = resident * fp.warps_per_cta;
+    const std::int64_t r = warps % slots;
+    rest.frame_begin = fp.mi0 + (warps - r) * GEO::FPW;
+    if (r > 0 && small_can_take(rest)) {
+      small_rest = true;
+      mi1_fast = rest.frame_begin;
+    }
+  }
+  const bool edges = p.nblocks == 0 && (fp.mi0 > p.frame_begin || (!small_rest && fp.mi1 < p.frame_end));
+  const bool small_edges = blocks <= resident && fp.warps_per_cta < 12;
+  SideStream* side = nullptr;
+  if (edges) {
+    side = side_stream();
+    if (!side) return cudaErrorUnknown;
+    if (cudaError_t err = cudaEventRecord(side->fork, stream); err != cudaSuccess) return err;
+    if (cudaError_t err = cudaStreamWaitEvent(side->s, side->fork, 0); err != cudaSuccess) return err;
+  }
+  auto edge = [&](const DecodeLaunch& ed) {
+    cudaError_t err = cudaSuccess;
+    if (small_edges && small_launch_wanted(ed) && try_small(ed, side->s, &err)) return err;
+    return launch_generic_i8(ed, side->s);
+  };
+  if (edges && fp.mi0 > p.frame_begin) {
+    DecodeLaunch ed = p;
+    ed.frame_end = fp.mi0;
+    if (cudaError_t err = edge(ed); err != cudaSuccess) return err;
+  }
+  if (edges && !small_rest && fp.mi1 < p.frame_end) {
+    DecodeLaunch ed = p;
+    ed.frame_begin = fp.mi1;
+    if (p.sigma) ed.sigma = static_cast<std::int64_t*>(p.sigma) + (fp.mi1 - p.frame_begin) * p.s;
+    if (cudaError_t err = edge(ed); err != cudaSuccess) return err;
+  }
+  if (edges) {
+    if (cudaError_t err = cudaEventRecord(side->join, side->s); err != cudaSuccess) return err;
+  }
+  FastParams fpl = fp;
+  fpl.mi1 = mi1_fast;
+  blocks = std::min<std::int64_t>(blocks, resident);
   if (fp.g_rows > 0) {
     // stream-ordered scratch for the spilled survivor rows (the pool keeps it
     // cached across launches, see retain_async_pool())
@@ -323,6 +360,7 @@ cudaError_t launch_variant(const DecodeLaunch& p, cudaStream_t stream, KSel ksel
     const cudaError_t ef = cudaFreeAsync(head_buf, stream);
     if (e == cudaSuccess) e = ef;
   }
+  if (e == cudaSuccess && small_rest && !try_small(rest, stream, &e)) e = cudaErrorNotSupported;
   if (e == cudaSuccess && edges) e = cudaStreamWaitEvent(stream, side->join, 0);
   return e;
 }

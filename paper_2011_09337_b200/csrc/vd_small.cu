@@ -86,6 +86,10 @@ bool plan_small(const DecodeLaunch& p, SmallLaunch* out) {
   wpc = std::max(wpc, 1);
   while (wpc > 1 && smem * wpc > kSmallSmemMax) --wpc;
   if (smem * wpc > kSmallSmemMax) return false;
+  // one round of CTAs only: beyond that the 16-states-per-lane kernel in one
+  // round of 4- / 8-warp CTAs is faster (2^21 stages: 75.6 -> see
+  // profiles/r02_ab_notes.md), and its edge frames come back here
+  if ((warps + wpc - 1) / wpc > sms) return false;
   sl.warps_per_cta = wpc;
   sl.smem_per_warp = smem;
   // every output word written whole by one task: frame and subframe
@@ -181,6 +185,18 @@ bool try_small(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
   }
   if (K7a::matches(p.k, p.b, p.polys) || K7b::matches(p.k, p.b, p.polys)) return false;
   return jit_small(p, stream, err, false, nullptr);
+}
+
+bool small_can_take(const DecodeLaunch& p) {
+  const char* env = std::getenv("VITDEC_SMALL");
+  if (env && std::atoi(env) == 0) return false;
+  if (p.nblocks > 0 || p.sigma || p.frame_list || p.b != 2) return false;
+  SmallLaunch sl;
+  int code = -1;
+  if (plan_any(p, &sl, &code)) return true;
+  if (K7a::matches(p.k, p.b, p.polys) || K7b::matches(p.k, p.b, p.polys)) return false;
+  bool whole = false;
+  return jit_small(p, nullptr, nullptr, true, &whole);
 }
 
 bool small_writes_whole_words(const DecodeLaunch& p) {

@@ -512,3 +512,36 @@ def test_random_geometry_mid_sizes_vs_oracle(code, port):
         torch.cuda.synchronize()
         got2 = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
         assert np.array_equal(got2, exp), (code, n, cfg, "device", np.flatnonzero(got2 != exp)[:8])
+
+
+@pytest.mark.parametrize("code", [K7, (7, 2, [0o165, 0o117])], ids=["K7a", "K7jit"])
+def test_round_split_sizes_vs_oracle(code, port):
+    """Mid-size launches where the 16-states-per-lane kernel runs one round
+    of 4- / 8-warp CTAs with its edge frames on the small-launch kernel beside
+    it, and multi-round launches whose partial last round (a few frame groups)
+    goes to the small kernel after it together with the tail edge frames
+    (csrc/vd_fast.cuh launch_variant): bit-exact vs the oracle, decoded into a
+    stale output buffer, over the sizes around those splits."""
+    import torch
+
+    from paper_2011_09337_b200.device import decode_i8_device
+
+    k, b, polys = code
+    t = trellis(k, b, polys)
+    sms = torch.cuda.get_device_properties(0).multi_processor_count
+    slots = 12 * sms  # 16-frame groups per round of 12-warp CTAs
+    rng = np.random.default_rng(777 + polys[0])
+    cases = []
+    for f, v1, v2, f0 in ((256, 20, 20, 0), (320, 20, 45, 32)):
+        for groups in (2 * sms + 5, 7 * sms, slots + 1, slots + 250):  # one round (4 / 8 warps); round + remainder
+            cases.append((vd.FrameConfig(f, v1, v2, f0), groups * 16 * f - int(rng.integers(1, f))))
+    for i, (cfg, n) in enumerate(cases):
+        rx, _ = port.gen_bench_block(k, b, polys, n, 2.5, 4000 + i)
+        q = oracle.quantize(rx, 32.0)
+        exp, _, _ = port.framed_decode(k, b, polys, q, n, cfg.f, cfg.v1, cfg.v2, cfg.f0)
+        out = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        decode_i8_device(t, cfg, n, torch.from_numpy(q).cuda(), 0, 0, -(-n // cfg.f), out, 0)
+        torch.cuda.synchronize()
+        got = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
+        bad = np.flatnonzero(got != exp)
+        assert bad.size == 0, (code, cfg, n, bad[:8], bad.size)
