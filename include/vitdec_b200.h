@@ -207,10 +207,15 @@ vd_status vd_depuncture_i8_device(const vd_puncture* pattern, const int8_t* punc
 vd_status vd_decode_punctured_i8(const vd_code* code, const vd_frame_cfg* cfg, const vd_puncture* pattern,
                                  const int8_t* punctured, int64_t n_punctured, uint32_t* out_packed, vd_stats* stats,
                                  const vd_exec* exec);
-/* Device-resident form: llr_scratch_dev (4-byte aligned, n_stages * b bytes,
- * see vd_depuncture_stages) receives the depunctured block, then every frame
- * is decoded into out_dev (ceil(n_stages / 32) words). Asynchronous; stats
- * (may be NULL) is computed on the host. */
+/* Device-resident form: every frame is decoded into out_dev (ceil(n_stages
+ * / 32) words). For the r2/3 ("11;10") and r3/4 ("110;101") patterns of the
+ * K=7 (171,133) code with f0 = 0 and a 4-byte aligned punctured_dev, the
+ * depuncture is fused into the fast kernel's LLR staging (the depunctured
+ * block never reaches HBM; llr_scratch_dev holds only the edge frames'
+ * windows); otherwise, or with VITDEC_PUNCT_FUSED=0, llr_scratch_dev
+ * (4-byte aligned, n_stages * b bytes, see vd_depuncture_stages) receives the
+ * depunctured block first. Asynchronous; stats (may be NULL) is computed on
+ * the host. */
 vd_status vd_decode_punctured_i8_device(const vd_code* code, const vd_frame_cfg* cfg, const vd_puncture* pattern,
                                         const int8_t* punctured_dev, int64_t n_punctured, int8_t* llr_scratch_dev,
                                         uint32_t* out_dev, vd_stats* stats, int32_t device, void* stream);
