@@ -114,9 +114,43 @@ bool fast_path_supported(const DecodeLaunch& p) {
          try_group_k568(p, nullptr, &unused, true) || try_jit(p, nullptr, &unused, true);
 }
 
+namespace fast {
+namespace {
+template <int K, class PN>
+bool try_jit_punct_pn(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
+                      std::int64_t* mi1) {
+  return try_punct_with<PlanCode<K, 2>, 16, PN>(p, stream, err, mi0, mi1, [&](cudaError_t* e) {
+    return jit::punct_kernel(p.k, p.polys, pattern, e);
+  });
+}
+
+template <int K>
+bool try_jit_punct_k(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
+                     std::int64_t* mi1) {
+  if (pattern == 23) return try_jit_punct_pn<K, PunctR23>(p, pattern, stream, err, mi0, mi1);
+  if (pattern == 34) return try_jit_punct_pn<K, PunctR34>(p, pattern, stream, err, mi0, mi1);
+  return false;
+}
+
+// Fused depuncture for the other K = 7 rate-1/2 codes: a run-time
+// instantiation of the same kernel ((133,171) r3/4: 1.03x the separate pass +
+// decode). Not for K = 5 / 6 (64 / 32 frames per warp: more than the fills'
+// two lanes per frame slot cover, plan()), nor K >= 8: there the decode costs
+// 2-4x more per bit, the separate pass is a smaller share than the fused
+// staging's per-block cost (K = 9 (561,753): fused 0.94x,
+// profiles/r02_ab_notes.md).
+bool try_jit_punct(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
+                   std::int64_t* mi1) {
+  if (p.b != 2 || p.k != 7 || !jit_code(p)) return false;
+  return try_jit_punct_k<7>(p, pattern, stream, err, mi0, mi1);
+}
+}  // namespace
+}  // namespace fast
+
 bool launch_fast_punct_i8(const DecodeLaunch& p, int pattern, cudaStream_t stream, cudaError_t* err,
                           std::int64_t* mi0, std::int64_t* mi1) {
-  return fast::try_punct_k7(p, pattern, stream, err, mi0, mi1);
+  if (fast::K7a::matches(p.k, p.b, p.polys)) return fast::try_punct_k7(p, pattern, stream, err, mi0, mi1);
+  return fast::try_jit_punct(p, pattern, stream, err, mi0, mi1);
 }
 
 cudaError_t side_fork(cudaStream_t main, cudaStream_t* side) {

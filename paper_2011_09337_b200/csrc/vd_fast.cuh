@@ -90,6 +90,7 @@ template <class C, int R, class PN = NoPunct>
 bool plan(const DecodeLaunch& p, Plan* out, bool pad_head = false) {
   using GEO = Geo<C, R>;
   if (PN::kActive && (GEO::B != 2 || pad_head || p.nblocks > 0 || p.llr_stage0 != 0 || p.sigma)) return false;
+  if (PN::kActive && 2 * GEO::FPW > 32) return false;  // fills: two lanes per frame slot
   FastParams fp{};
   fp.llr_head = p.llr_head;
   fp.head_pitch = p.head_pitch;
@@ -378,11 +379,12 @@ bool try_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err) {
 /// 0 at byte 0); the fast kernel decodes the interior frames [*mi0, *mi1)
 /// it can take, the caller decodes the rest from a dense copy. Returns false
 /// (nothing launched) when the plan needs more than TMEM + shared memory.
-template <class C, int R, class PN>
-bool try_punct_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
-                       std::int64_t* mi1) {
+// Fused-depuncture launch of code class C's plan with the kernel kfn(&err)
+// returns (precompiled or run-time instantiated).
+template <class C, int R, class PN, class KFn>
+bool try_punct_with(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
+                    std::int64_t* mi1, KFn kfn) {
   using GEO = Geo<C, R>;
-  if (!C::matches(p.k, p.b, p.polys)) return false;
   if (p.f % PN::P || p.v1 % PN::P || p.v2 % PN::P) return false;
   Plan pl;
   if (!plan<C, R, PN>(p, &pl) || !pl.tm || pl.gl) return false;
@@ -390,18 +392,33 @@ bool try_punct_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* 
   *mi1 = pl.fp.mi1;
   if (!stream && !err) return true;  // probe
   const FastParams& fp = pl.fp;
-  auto kern = fast_kernel<C, R, true, false, PN>;
-  cudaError_t e = allow_max_smem(reinterpret_cast<const void*>(kern));
+  cudaError_t e = cudaSuccess;
+  const void* kern = kfn(&e);
+  if (!kern) {
+    *err = e != cudaSuccess ? e : cudaErrorInvalidSource;
+    return true;
+  }
+  e = allow_max_smem(kern);
   if (e == cudaSuccess) {
     const std::int64_t warps = (fp.mi1 - fp.mi0 + GEO::FPW - 1) / GEO::FPW;
     std::int64_t blocks = (warps + fp.warps_per_cta - 1) / fp.warps_per_cta;
     blocks = std::min<std::int64_t>(blocks, static_cast<std::int64_t>(sm_count()));
-    kern<<<static_cast<unsigned>(blocks), fp.warps_per_cta * 32, pl.smem, stream>>>(fp);
+    FastParams fpl = fp;
+    void* args[] = {&fpl};
+    e = cudaLaunchKernel(kern, dim3(static_cast<unsigned>(blocks)), dim3(fp.warps_per_cta * 32), args, pl.smem, stream);
     note_launch();
-    e = cudaGetLastError();
   }
   *err = e;
   return true;
+}
+
+template <class C, int R, class PN>
+bool try_punct_variant(const DecodeLaunch& p, cudaStream_t stream, cudaError_t* err, std::int64_t* mi0,
+                       std::int64_t* mi1) {
+  if (!C::matches(p.k, p.b, p.polys)) return false;
+  return try_punct_with<C, R, PN>(p, stream, err, mi0, mi1, [](cudaError_t*) {
+    return reinterpret_cast<const void*>(fast_kernel<C, R, true, false, PN>);
+  });
 }
 
 }  // namespace fast

@@ -56,6 +56,8 @@ bool enabled();
 const void* fast_kernel(int k, int b, const std::uint32_t* polys, bool tm, bool gl, cudaError_t* err);
 /// The small-launch kernel (vd_small_dev.cuh, 8 states per lane) for a rate-1/2 code.
 const void* small_kernel(int k, const std::uint32_t* polys, cudaError_t* err);
+/// Fused-depuncture fast kernel (pattern 23: PunctR23, 34: PunctR34) of a B = 2 code.
+const void* punct_kernel(int k, const std::uint32_t* polys, int pattern, cudaError_t* err);
 const std::string& last_log();
 /// Compile only (no GPU needed): false + last_log() on failure.
 bool compile_check(int k, int b, const std::uint32_t* polys);

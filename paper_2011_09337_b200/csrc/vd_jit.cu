@@ -202,6 +202,13 @@ const void* fast_kernel(int k, int b, const std::uint32_t* polys, bool tm, bool 
   return kernel(expression(k, b, polys, tm, gl), err);
 }
 
+const void* punct_kernel(int k, const std::uint32_t* polys, int pattern, cudaError_t* err) {
+  if (pattern != 23 && pattern != 34) return nullptr;
+  return kernel("&vd::fast::fast_kernel<" + code_type(k, 2, polys) + ", 16, true, false, vd::fast::PunctR" +
+                    std::to_string(pattern) + ">",
+                err);
+}
+
 const void* small_kernel(int k, const std::uint32_t* polys, cudaError_t* err) {
   return kernel("&vd::fast::small_kernel<" + code_type(k, 2, polys) + ", 8>", err);
 }

@@ -250,20 +250,31 @@ def test_drop_in_depuncture_f64_matches_reference(name):
         assert np.array_equal(got, out[:n_stages.value * b]), (name, n_p)
 
 
+FUSED_CASES = [(K7, "r23", (256, 20, 20)), (K7, "r23", (128, 16, 42)), (K7, "r34", (255, 21, 21)),
+               (K7, "r34", (240, 24, 48)),
+               # other rate-1/2 codes: run-time instantiations of the fused kernel
+               ((7, 2, [0o133, 0o171]), "r23", (256, 20, 20)), ((9, 2, [0o561, 0o753]), "r34", (240, 45, 45)),
+               ((5, 2, [0o23, 0o35]), "r23", (128, 16, 24)),  # K != 7: the separate pass
+               ((8, 2, [0o247, 0o170]), "r34", (252, 30, 30))]
+
+
 @pytest.mark.gpu
-@pytest.mark.parametrize("pattern,cfg", [("r23", (256, 20, 20)), ("r23", (128, 16, 42)), ("r34", (255, 21, 21)),
-                                         ("r34", (240, 24, 48))])
-def test_fused_depuncture_device_decode(pattern, cfg, monkeypatch):
-    """Depuncture fused into the fast kernel's LLR staging (vd_fast.cuh
+@pytest.mark.parametrize("code,pattern,cfg", FUSED_CASES,
+                         ids=[f"K{c[0]}_{c[2][0]:o}_{p}_{g[0]}" for c, p, g in FUSED_CASES])
+def test_fused_depuncture_device_decode(code, pattern, cfg, monkeypatch, tmp_path):
+    """Depuncture fused into the fast kernel's LLR staging (vd_fast_dev.cuh
     Punct: the kernel gathers the punctured stream into its shared-memory LLR
-    ring, re-inserting the zeros) == the oracle's framed_decode of the
-    depunctured block, and == the separate-pass path (VITDEC_PUNCT_FUSED=0);
-    edge frames come from dense copies of their windows."""
+    ring, re-inserting the zeros; the default) == the oracle's framed_decode
+    of the depunctured block, and == the separate-pass path
+    (VITDEC_PUNCT_FUSED=0); edge frames come from dense copies of their
+    windows. The fused kernel is checked to be the one that ran."""
     import ctypes as C
 
     import torch
+    from torch.profiler import ProfilerActivity, profile
 
-    k, b, polys = K7
+    monkeypatch.setenv("VITDEC_JIT_CACHE", str(tmp_path))
+    k, b, polys = code
     rows = _rows(pattern)
     t = vd.build_trellis(vd.CodeSpec(k, b, polys))
     p = vd.PuncturePattern.parse(rows)
@@ -280,10 +291,16 @@ def test_fused_depuncture_device_decode(pattern, cfg, monkeypatch):
             out = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")  # stale bits must be cleared
             s = vd.api.VdStats()
             c, pc = fc.to_c(), p.to_c()
-            vd.api.check(vd.lib().vd_decode_punctured_i8_device(t.handle, C.byref(c), C.byref(pc), dev_in.data_ptr(),
-                                                                punct.size, scratch.data_ptr(), out.data_ptr(),
-                                                                C.byref(s), -1, None))
-            torch.cuda.synchronize()
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                vd.api.check(vd.lib().vd_decode_punctured_i8_device(t.handle, C.byref(c), C.byref(pc),
+                                                                    dev_in.data_ptr(), punct.size, scratch.data_ptr(),
+                                                                    out.data_ptr(), C.byref(s), -1, None))
+                torch.cuda.synchronize()
+            if n_stages == 1 << 20:
+                ran = [e.name for e in prof.events() if e.device_type.name == "CUDA"]
+                # (odd f or v1: the fast kernel needs 4-byte aligned frame windows, plan())
+                takes_fused = fused == "1" and cfg[0] % 2 == 0 and cfg[1] % 2 == 0 and k == 7
+                assert any("Punct<" in x for x in ran) == takes_fused, (fused, ran)
             res[fused] = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
             assert (s.frames, s.stages, s.tracebacks) == st
         bad = np.flatnonzero(res["1"] != exp)

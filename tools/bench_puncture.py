@@ -29,6 +29,9 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--e2e-stages", type=int, default=1 << 28)
+    ap.add_argument("--k", type=int, default=7)
+    ap.add_argument("--polys", default="171,133", help="octal generators of the rate-1/2 mother code")
+    ap.add_argument("--frame", default="240,24,24", help="f,v1,v2 (multiples of the periods 2 and 3)")
     a = ap.parse_args()
 
     import numpy as np
@@ -41,8 +44,8 @@ def main():
 
     peaks = json.loads((ROOT / "MEASURED_PEAKS.json").read_text()) if (ROOT / "MEASURED_PEAKS.json").exists() else {
         "hbm_gbs": 6650.0}
-    t = vd.build_trellis(vd.CodeSpec(7, 2, [0o171, 0o133]))
-    cfg = vd.FrameConfig(240, 24, 24)  # f, v1, v2 multiples of the periods 2 and 3 (decoder.cpp:14-19)
+    t = vd.build_trellis(vd.CodeSpec(a.k, 2, [int(x, 8) for x in a.polys.split(",")]))
+    cfg = vd.FrameConfig(*[int(x) for x in a.frame.split(",")])  # multiples of the periods 2 and 3 (decoder.cpp:14-19)
     n = a.stages
     s = torch.cuda.Stream()
     full = torch.empty(n * 2, dtype=torch.int8, device="cuda")
@@ -114,7 +117,7 @@ def main():
                                                                      host_out.data_ptr(), C.byref(st), None)))
         dep_bytes = punct_h.size + n * 2
         print(json.dumps({
-            "pattern": name, "stages": n, "cfg": "f=240 v1=24 v2=24 (period-aligned)",
+            "pattern": name, "stages": n, "code": f"K={a.k} ({a.polys})", "cfg": f"f,v1,v2={a.frame} (period-aligned)",
             "depuncture": {"ms": dep_s * 1e3, "GBps": dep_bytes / dep_s / 1e9, "hbm_peak": peaks["hbm_gbs"],
                            "frac": dep_bytes / dep_s / 1e9 / peaks["hbm_gbs"], "bytes": dep_bytes,
                            "matches_oracle": ok_dep},
