@@ -545,3 +545,10 @@ def test_round_split_sizes_vs_oracle(code, port):
         got = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
         bad = np.flatnonzero(got != exp)
         assert bad.size == 0, (code, cfg, n, bad[:8], bad.size)
+        if i % 4 == 3:
+            # host streaming in chunks whose decodes split the same way (each
+            # chunk's window starts inside the stream: llr_stage0 > 0)
+            chunk = (slots + 100) * 16 * cfg.f
+            packed, _ = vd.framed_decode_stream(q, n, t, cfg, chunk_stages=chunk)
+            got = vd.unpack_bits(packed, n)
+            assert np.array_equal(got, exp), (code, cfg, n, "chunked", np.flatnonzero(got != exp)[:8])
