@@ -450,6 +450,45 @@ def test_small_launch_kernel_vs_oracle(polys, port, monkeypatch):
             assert (stats.frames, stats.stages, stats.tracebacks) == st
 
 
+@pytest.mark.parametrize("inputs", ["noise", "saturated", "minus3dB_scale1", "3dB"])
+def test_small_launch_extreme_inputs_vs_oracle(inputs, port, monkeypatch):
+    """The small kernel (lagged renormalisation: metrics must stay inside
+    int16 over 12 stages of growth) on pure-noise, saturated (+-127 only) and
+    -3 dB tie-heavy (scale 1) LLRs as well as 3 dB ones, over frame
+    geometries with whole-word output (so the output is not pre-zeroed);
+    bit-exact vs the oracle through the host and the device calls."""
+    import torch
+
+    from paper_2011_09337_b200.device import decode_i8_device
+
+    k, b, polys = K7
+    t = trellis(k, b, polys)
+    rng = np.random.default_rng({"noise": 1, "saturated": 4, "minus3dB_scale1": 2, "3dB": 3}[inputs])
+    cfgs = [(256, 20, 20), (128, 0, 0), (512, 42, 42), (160, 5, 9), (256, 3, 63), (416, 30, 2)]
+    for i, (f, v1, v2) in enumerate(cfgs):
+        n = 32 * int(rng.integers(2_000, 20_000))
+        if inputs == "noise":
+            q = rng.integers(-127, 128, size=b * n, dtype=np.int8)
+        elif inputs == "saturated":
+            q = (rng.integers(0, 2, size=b * n, dtype=np.int8) * 2 - 1) * np.int8(127)
+        else:
+            rx, _ = port.gen_bench_block(k, b, polys, n, -3.0 if inputs != "3dB" else 3.0, 700 + i)
+            q = oracle.quantize(rx, 1.0 if inputs != "3dB" else 32.0)
+        q = q.astype(np.int8)
+        exp, st, _ = port.framed_decode(k, b, polys, q, n, f, v1, v2, 0)
+        cfg = vd.FrameConfig(f, v1, v2)
+        monkeypatch.setenv("VITDEC_SMALL", "1")
+        packed, stats = vd.framed_decode_stream(q, n, t, cfg)
+        got = vd.unpack_bits(packed, n)
+        assert np.array_equal(got, exp), (inputs, n, cfg, np.flatnonzero(got != exp)[:8])
+        assert (stats.frames, stats.stages, stats.tracebacks) == st
+        out = torch.full(((n + 31) // 32,), -1, dtype=torch.int32, device="cuda")
+        decode_i8_device(t, cfg, n, torch.from_numpy(q).cuda(), 0, 0, -(-n // f), out, 0)
+        torch.cuda.synchronize()
+        got2 = vd.unpack_bits(out.cpu().numpy().view(np.uint32), n)
+        assert np.array_equal(got2, exp), (inputs, n, cfg, "device", np.flatnonzero(got2 != exp)[:8])
+
+
 @pytest.mark.parametrize("cfg", [(256, 20, 20, 0), (320, 20, 45, 32), (256, 20, 20, 0, 7)],
                          ids=["f256", "f320f0_32", "n_unaligned"])
 def test_small_launch_whole_words_over_stale_output(cfg, port):
