@@ -574,7 +574,12 @@ def run_ours(args):
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_gbps, "unit": "Gbps", "h2d_bytes_per_step": ne * B * world,
                     "d2h_bytes_per_step": ((ne + 31) // 32) * 4 * world, "info_bits_per_step": ne * world,
-                    "matches_device_decode": same},
+                    "matches_device_decode": same,
+                    # PCIe: H2D GB/s this line moved (ne bits at e2e_gbps -> ne * B bytes per
+                    # ne / e2e_gbps ns), against the box's pinned-copy ceiling measured by
+                    # tools/pcie_probe.py (profiles/r02_pcie_probe.json)
+                    "h2d_gbs": (B * e2e_gbps / world) if e2e_gbps else None,
+                    "h2d_ceiling_gbs": _pcie_ceiling()},
             "gpu_launches": int(round(launches * args.steps)),
             "gpu_launches_per_step_per_rank": launches,
             "clocks": clocks,
@@ -589,6 +594,14 @@ def run_ours(args):
         dist.barrier()
         dist.destroy_process_group()
     return result
+
+
+def _pcie_ceiling():
+    """Pinned H2D GB/s of this box type (tools/pcie_probe.py), or None."""
+    try:
+        return json.loads((ROOT / "profiles" / "r02_pcie_probe.json").read_text())["h2d_one_copy_GBps"]
+    except (OSError, ValueError, KeyError):
+        return None
 
 
 def main():
