@@ -151,13 +151,20 @@ bool int8_exact(const LlrBlock& llr, std::int8_t* out, int workers) {
 // A BitVec of n bytes whose pages are already faulted in. A fresh multi-MiB
 // vector is an mmap, and first-touch faults in the single-threaded zero-fill
 // of std::vector's constructor cost more than the decode (2^26 bits: 23 ms);
-// `workers` threads fault their own ranges in first (MADV_POPULATE_WRITE).
+// its 2 MiB-aligned interior is advised to huge pages, then `workers` threads
+// fault their own ranges in first (MADV_POPULATE_WRITE).
 BitVec resident_bits(Eigen::Index n, int workers) {
   BitVec bits;
   bits.reserve(static_cast<std::size_t>(n));
   constexpr std::uintptr_t kPage = 4096;
   if (n >= (std::int64_t{4} << 20)) {
     const auto base = reinterpret_cast<std::uintptr_t>(bits.data());
+    {  // 2 MiB pages where transparent huge pages are on "madvise": 512x fewer
+       // faults (reference-API e2e at 2^26 bits 2.2 -> 2.6 Gbps; advisory)
+      constexpr std::uintptr_t kHuge = std::uintptr_t{2} << 20;
+      const std::uintptr_t a = (base + kHuge - 1) & ~(kHuge - 1), b = (base + n) & ~(kHuge - 1);
+      if (b > a) madvise(reinterpret_cast<void*>(a), b - a, MADV_HUGEPAGE);
+    }
     host_parallel(n, workers, [&](std::int64_t lo, std::int64_t hi) {
       const std::uintptr_t a = (base + lo + kPage - 1) & ~(kPage - 1), b = (base + hi) & ~(kPage - 1);
       if (b > a) madvise(reinterpret_cast<void*>(a), b - a, kMadvPopulateWrite);  // (advisory: failure is harmless)
