@@ -6,6 +6,8 @@
 #include <algorithm>
 #include <array>
 #include <atomic>
+#include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -341,13 +343,24 @@ DecodeOutput framed_decode(const LlrBlock& llr, const Trellis& trellis, const Fr
   DecodeOutput out;
   Background prep([&out, n, workers] { out.bits = resident_bits(n, std::max(1, workers / 4)); });
   // `workers` host threads prepare the block / unpack the bits (the GPU does the decode)
-  if (int8_exact(llr, q, workers)) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const bool i8 = int8_exact(llr, q, workers);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (i8) {
     check(vd_decode_i8(trellis.native(), &c, q, n, packed, &st, &ex));
   } else {
     check(vd_decode_f64(trellis.native(), &c, llr.data(), n, packed, &st, &ex));
   }
+  const auto t2 = std::chrono::steady_clock::now();
   prep.wait();
+  const auto t3 = std::chrono::steady_clock::now();
   unpack_into(out.bits, packed, n, workers);
+  const auto t4 = std::chrono::steady_clock::now();
+  if (std::getenv("VITDEC_DROPIN_TIMING")) {  // (phase breakdown on stderr)
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    std::fprintf(stderr, "dropin: convert %.2f decode %.2f wait-pages %.2f unpack %.2f ms\n", ms(t0, t1), ms(t1, t2),
+                 ms(t2, t3), ms(t3, t4));
+  }
   out.stats = from_c(st);
   return out;
 }
