@@ -1022,9 +1022,18 @@ __global__ void __launch_bounds__(max_warps<C>() * 32, 1) fast_kernel(const Fast
         ++rc;
       }
     } else {
-      run_block<C, GEO, MD, TM, GL, BUF, PN>(st, blk, bc, tprev, pfA, pfB, 0u, rec);
-      pfA += WPB;
-      pfB += WPB;
+      if constexpr (C::kK == 7 && GEO::B == 2) {
+        // prefetch address = the lane's window base + a warp-uniform block
+        // offset (K=7 r1/2: 328 instead of 332 instructions per TMEM block,
+        // C5 123.1 vs 122.3 Gbps; K=9 and B=3 measured 0.3-0.9 % slower this
+        // way, profiles/r02_ab_notes.md)
+        const int pfo = (blk + 2) * WPB;
+        run_block<C, GEO, MD, TM, GL, BUF, PN>(st, blk, bc, tprev, llrA + pfo, llrB + pfo, 0u, rec);
+      } else {
+        run_block<C, GEO, MD, TM, GL, BUF, PN>(st, blk, bc, tprev, pfA, pfB, 0u, rec);
+        pfA += WPB;
+        pfB += WPB;
+      }
     }
     block_end(blk, buf_tag);
   };
